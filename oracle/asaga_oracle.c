@@ -1,0 +1,281 @@
+/*
+ * oracle/asaga_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, sequential fp64 CPU implementation of what the ASAGA hot
+ * path computes, written from the paper (Leblond, Pedregosa, Lacoste-Julien,
+ * "ASAGA: Asynchronous Parallel SAGA", arXiv 1606.04809; /root/reference/PAPER.md,
+ * cited below as P:<line>).  It exists to check the CUDA path and nothing else:
+ * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load it.  It shares no code, header, table or constant
+ * generator with paper_1606_04809_b200/csrc (which has its own Philox, its own
+ * index map, its own column-count pass, ...).
+ *
+ * Compiled with -O2 -ffp-contract=off (no FMA contraction, no fast-math):
+ * every sum is sequential in CSR order.  No blocking, fusion or reordering.
+ *
+ * Pinned by tests/test_oracle_pins.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* Sampler (reading R2; the paper only says "uniformly at random",
+ * P:243).  Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11), written
+ * out round by round:  one round maps (c0,c1,c2,c3) with key (k0,k1) to
+ *   (hi(M1*c2) ^ c1 ^ k0,  lo(M1*c2),  hi(M0*c0) ^ c3 ^ k1,  lo(M0*c0))
+ * and the key is bumped by the Weyl constants between rounds.              */
+#define ORACLE_PHILOX_M0 0xD2511F53u
+#define ORACLE_PHILOX_M1 0xCD9E8D57u
+#define ORACLE_PHILOX_W0 0x9E3779B9u
+#define ORACLE_PHILOX_W1 0xBB67AE85u
+
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2],
+                          uint32_t out[4]) {
+  uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+  uint32_t k0 = key_in[0], k1 = key_in[1];
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) {
+      k0 += ORACLE_PHILOX_W0;
+      k1 += ORACLE_PHILOX_W1;
+    }
+    uint64_t p0 = (uint64_t)ORACLE_PHILOX_M0 * (uint64_t)c0;
+    uint64_t p1 = (uint64_t)ORACLE_PHILOX_M1 * (uint64_t)c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0;
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c3 ^ k1;
+    uint32_t n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* i_t = floor(r * n / 2^64), r = (out1 << 32) | out0, counter (lo32 t, hi32 t, 0, 0),
+ * key (lo32 seed, hi32 seed).  Uniform on {0..n-1} up to bias n/2^64 (reading R2).
+ * "Sample i uniformly at random" happens before any read (Alg. 2 line 3). */
+uint64_t oracle_sample_index(uint64_t seed, uint64_t t, uint64_t n) {
+  uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32), 0u, 0u};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t out[4];
+  oracle_philox4x32_10(ctr, key, out);
+  uint64_t r = ((uint64_t)out[1] << 32) | (uint64_t)out[0];
+  unsigned __int128 prod = (unsigned __int128)r * (unsigned __int128)n;
+  return (uint64_t)(prod >> 64);
+}
+
+/* Raw Philox words for counters (lo32 t, hi32 t, 0, 0), t = t0..t0+count-1. */
+void oracle_philox_stream(uint64_t seed, uint64_t t0, uint64_t count, uint32_t* out) {
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (uint64_t k = 0; k < count; ++k) {
+    uint64_t t = t0 + k;
+    uint32_t ctr[4] = {(uint32_t)t, (uint32_t)(t >> 32), 0u, 0u};
+    oracle_philox4x32_10(ctr, key, out + 4 * k);
+  }
+}
+
+void oracle_sample_stream(uint64_t seed, uint64_t t0, uint64_t count, uint64_t n,
+                          int64_t* out) {
+  for (uint64_t k = 0; k < count; ++k) out[k] = (int64_t)oracle_sample_index(seed, t0 + k, n);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Sparsity profile ("D ... coefficients 1/p_v ... p_v is the
+ * probability that dimension v belongs to S_i"; "first pass").
+ * n_v = #{i : v in S_i}; S_i = the stored entries of row i (reading R3).   */
+void oracle_column_counts(int64_t n, int64_t d, const int64_t* indptr,
+                          const int32_t* indices, int64_t* counts) {
+  for (int64_t v = 0; v < d; ++v) counts[v] = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) counts[indices[k]] += 1;
+}
+
+/* D_v = 1/p_v = n / n_v (IEEE division); D_v = 0 when n_v = 0 (reading R4). */
+void oracle_reweight(int64_t n, int64_t d, const int64_t* counts, double* D) {
+  for (int64_t v = 0; v < d; ++v)
+    D[v] = counts[v] > 0 ? (double)n / (double)counts[v] : 0.0;
+}
+
+/* L = max_i ||a_i||^2 / 4 + lambda: the smoothness constant of the logistic f_i
+ * plus the l2 term ("L-Lipschitz", Table 1 L=0.25 for normalised RCV1). */
+double oracle_lipschitz(int64_t n, const int64_t* indptr, const double* data,
+                        double lambda) {
+  double best = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double sq = 0.0;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) sq += data[k] * data[k];
+    if (sq > best) best = sq;
+  }
+  return best / 4.0 + lambda;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Logistic pieces (Section 4.1).
+ * f_i(x) = log(1 + exp(-b_i a_i^T x)); f_i'(x) = sigma_i(x) a_i with
+ * sigma_i(x) = -b_i / (1 + exp(b_i a_i^T x)) (the scalar memory of App. E). */
+static double oracle_softplus(double m) { /* log(1+exp(m)), stable form */
+  double am = m < 0 ? -m : m;
+  return (m > 0 ? m : 0.0) + log1p(exp(-am));
+}
+
+double oracle_sigma(double b, double z) { return -b / (1.0 + exp(b * z)); }
+
+/* f(x) = (1/n) sum_i log(1+exp(-b_i a_i.x)) + (lambda/2)||x||^2. */
+double oracle_objective(int64_t n, int64_t d, const int64_t* indptr,
+                        const int32_t* indices, const double* data, const double* y,
+                        double lambda, const double* x) {
+  double loss = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double z = 0.0;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) z += data[k] * x[indices[k]];
+    loss += oracle_softplus(-y[i] * z);
+  }
+  double sq = 0.0;
+  for (int64_t v = 0; v < d; ++v) sq += x[v] * x[v];
+  return loss / (double)n + 0.5 * lambda * sq;
+}
+
+/* grad f(x) = (1/n) sum_i sigma_i(x) a_i + lambda x  (gradient of Eq. 1 with the
+ * l2 term of Section 4.1). */
+void oracle_full_grad(int64_t n, int64_t d, const int64_t* indptr,
+                      const int32_t* indices, const double* data, const double* y,
+                      double lambda, const double* x, double* g) {
+  for (int64_t v = 0; v < d; ++v) g[v] = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double z = 0.0;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) z += data[k] * x[indices[k]];
+    double s = oracle_sigma(y[i], z);
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) g[indices[k]] += s * data[k];
+  }
+  for (int64_t v = 0; v < d; ++v) g[v] = g[v] / (double)n + lambda * x[v];
+}
+
+/* ------------------------------------------------------------------------ */
+/* Sparse SAGA (Eq. 3) with the exact l2 term of Section 4.2
+ * (P:519-522), one sample at a time, in the order of Algorithm 2:
+ *   3: sample i                                (oracle_sample_index, before any read)
+ *   5: [x]_{S_i}; 6: alpha_i; 7: [abar]_{S_i}  (sequential: reads are exact)
+ *   8: dalpha = f_i'(x) - alpha_i              (scalar form, App. E)
+ *   9: dx = -gamma (dalpha a_i + D_i abar + lambda D_i x)
+ *  11: x_v += dx_v;  12: alpha_i += dalpha;  13: abar_v += dalpha a_iv / n
+ * Every term of u uses the pre-step x and abar (reading R8).  State (x, alpha,
+ * abar) is updated in place; updates t0 .. t0+T-1 use samples i_t.          */
+/* One Sparse SAGA step on sample i (lines 4-13 of Alg. 2 executed without
+ * interleaving).  u is scratch of at least |S_i| doubles. */
+void oracle_saga_step(int64_t n, const int64_t* indptr, const int32_t* indices,
+                      const double* data, const double* y, const double* D,
+                      double lambda, double gamma, int64_t i, double* x, double* alpha,
+                      double* alpha_bar, double* u) {
+  const double inv_n = 1.0 / (double)n;
+  int64_t lo = indptr[i], hi = indptr[i + 1];
+  double z = 0.0;
+  for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+  double s = oracle_sigma(y[i], z);
+  double dalpha = s - alpha[i];
+  for (int64_t k = lo; k < hi; ++k) {
+    int32_t v = indices[k];
+    u[k - lo] = dalpha * data[k] + D[v] * (alpha_bar[v] + lambda * x[v]);
+  }
+  for (int64_t k = lo; k < hi; ++k) {
+    int32_t v = indices[k];
+    x[v] = x[v] - gamma * u[k - lo];
+    alpha_bar[v] = alpha_bar[v] + dalpha * data[k] * inv_n;
+  }
+  alpha[i] = alpha[i] + dalpha;
+}
+
+void oracle_sparse_saga(int64_t n, int64_t d, const int64_t* indptr,
+                        const int32_t* indices, const double* data, const double* y,
+                        const double* D, double lambda, double gamma, uint64_t seed,
+                        uint64_t t0, uint64_t T, double* x, double* alpha,
+                        double* alpha_bar) {
+  (void)d;
+  int64_t maxrow = 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] - indptr[i] > maxrow) maxrow = indptr[i + 1] - indptr[i];
+  double* u = (double*)malloc(sizeof(double) * (size_t)maxrow);
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    oracle_saga_step(n, indptr, indices, data, y, D, lambda, gamma, i, x, alpha, alpha_bar, u);
+  }
+  free(u);
+}
+
+/* Same run, with the objective evaluated every eval_every updates (reading R12),
+ * written to f_trace[0..n_evals-1]; f_trace[j] is f after (j+1)*eval_every
+ * updates.  Returns the number of evaluations written. */
+int64_t oracle_sparse_saga_trace(int64_t n, int64_t d, const int64_t* indptr,
+                                 const int32_t* indices, const double* data,
+                                 const double* y, const double* D, double lambda,
+                                 double gamma, uint64_t seed, uint64_t t0,
+                                 uint64_t eval_every, int64_t n_evals, double* x,
+                                 double* alpha, double* alpha_bar, double* f_trace) {
+  for (int64_t j = 0; j < n_evals; ++j) {
+    oracle_sparse_saga(n, d, indptr, indices, data, y, D, lambda, gamma, seed,
+                       t0 + (uint64_t)j * eval_every, eval_every, x, alpha, alpha_bar);
+    f_trace[j] = oracle_objective(n, d, indptr, indices, data, y, lambda, x);
+  }
+  return n_evals;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Bounded-delay Sparse SAGA (NEXT-1 tool, Assumption 1 P:316-322 taken at its
+ * bound): update t reads x, alpha_i and abar as they stand after updates
+ * 0..t-tau-1 have been written, i.e. every update is applied tau steps after
+ * its read.  tau = 0 is exactly oracle_sparse_saga.  Used to predict the
+ * convergence knee in the number of in-flight samples.  Pending updates are
+ * kept in a ring of tau slots (each stores the row, dalpha and u).           */
+typedef struct {
+  int64_t i, lo, hi;
+  double dalpha;
+  double* u;
+} oracle_pending;
+
+void oracle_delayed_saga(int64_t n, int64_t d, const int64_t* indptr,
+                         const int32_t* indices, const double* data, const double* y,
+                         const double* D, double lambda, double gamma, uint64_t seed,
+                         uint64_t t0, uint64_t T, int64_t tau, double* x, double* alpha,
+                         double* alpha_bar) {
+  (void)d;
+  const double inv_n = 1.0 / (double)n;
+  int64_t maxrow = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] - indptr[i] > maxrow) maxrow = indptr[i + 1] - indptr[i];
+  int64_t slots = tau + 1;
+  oracle_pending* ring = (oracle_pending*)calloc((size_t)slots, sizeof(oracle_pending));
+  for (int64_t s = 0; s < slots; ++s) {
+    ring[s].u = (double*)malloc(sizeof(double) * (size_t)(maxrow > 0 ? maxrow : 1));
+    ring[s].i = -1;
+  }
+  for (uint64_t step = 0; step < T + (uint64_t)tau + 1; ++step) {
+    int64_t slot = (int64_t)(step % (uint64_t)slots);
+    /* write the update read tau steps ago (it occupies this slot) */
+    oracle_pending* p = &ring[slot];
+    if (p->i >= 0) {
+      for (int64_t k = p->lo; k < p->hi; ++k) {
+        int32_t v = indices[k];
+        x[v] = x[v] - gamma * p->u[k - p->lo];
+        alpha_bar[v] = alpha_bar[v] + p->dalpha * data[k] * inv_n;
+      }
+      alpha[p->i] = alpha[p->i] + p->dalpha;
+      p->i = -1;
+    }
+    if (step >= T) continue;
+    /* read + compute update t = t0 + step */
+    int64_t i = (int64_t)oracle_sample_index(seed, t0 + step, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double s = oracle_sigma(y[i], z);
+    double dalpha = s - alpha[i];
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      p->u[k - lo] = dalpha * data[k] + D[v] * (alpha_bar[v] + lambda * x[v]);
+    }
+    p->i = i; p->lo = lo; p->hi = hi; p->dalpha = dalpha;
+  }
+  for (int64_t s = 0; s < slots; ++s) free(ring[s].u);
+  free(ring);
+}
