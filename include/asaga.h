@@ -1,0 +1,215 @@
+/*
+ * asaga.h -- C-ABI of the B200 ASAGA hot path (libasaga.so).
+ *
+ * Problem (Leblond, Pedregosa, Lacoste-Julien, arXiv 1606.04809, Section 4.1,
+ * PAPER.md:483-486):
+ *     min_x f(x) = (1/n) sum_i log(1 + exp(-b_i a_i^T x)) + (lambda/2) ||x||^2
+ * solved by Sparse SAGA (Eq. 3) with the exact l2 term of
+ * Section 4.2, run as ASAGA (Algorithm 2):
+ * per sampled row i, with D_v = n / n_v,
+ *     dalpha = f_i'(x^) - alpha^_i                      (scalar memory, App. E)
+ *     x_v    += -gamma (dalpha a_iv + D_v abar^_v + lambda D_v x^_v)   v in S_i
+ *     alpha_i += dalpha ;  abar_v += dalpha a_iv / n                   v in S_i
+ * with lock-free, unsynchronised reads and atomic coordinate adds
+ * (Property 3).
+ *
+ * Conventions for every entry point:
+ *  - Host pointers are caller-owned and only borrowed for the duration of the
+ *    call unless stated otherwise.  "_dev" pointers are device pointers on the
+ *    context's device.  The library never frees caller memory.
+ *  - All floating point is IEEE fp64; indices are 0-based int32; row pointers int64.
+ *  - Every function returns an asaga_status; no C++ exception crosses the ABI.
+ *    After a failure asaga_last_error(ctx) (or asaga_last_error(NULL) when no
+ *    context exists, e.g. a failed asaga_init) returns a message naming the
+ *    offending row where one exists.
+ *  - One context per device per host thread; a context is not thread-safe.
+ *  - Blocking calls synchronise the context's stream before returning;
+ *    "_async" / "_device" calls only enqueue work on it.
+ */
+#ifndef ASAGA_H
+#define ASAGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASAGA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ASAGA_API __attribute__((visibility("default")))
+#else
+#define ASAGA_API
+#endif
+
+typedef struct asaga_ctx asaga_ctx;
+
+typedef enum {
+  ASAGA_OK = 0,
+  ASAGA_E_INVALID_ARG = 1, /* NULL pointer, lambda <= 0, gamma <= 0, n or d out of range */
+  ASAGA_E_BAD_CSR = 2,     /* indptr not monotone / not ending at nnz, empty row,
+                              index out of [0,d), indices not strictly increasing in a row,
+                              non-finite value (rows must be non-empty: SPEC S:24-27) */
+  ASAGA_E_BAD_LABEL = 3,   /* some y_i not in {-1, +1} (b_i in {-1,+1}) */
+  ASAGA_E_CUDA = 4,        /* a CUDA runtime error (message carries cudaGetErrorString) */
+  ASAGA_E_OOM = 5,         /* device allocation failed */
+  ASAGA_E_DIVERGED = 6,    /* non-finite iterate after asaga_run (divergence guard) */
+  ASAGA_E_STATE = 7        /* call not valid in the context's state (e.g. no sample record) */
+} asaga_status;
+
+/* A CSR matrix: row i holds indices[indptr[i] .. indptr[i+1]) (strictly
+ * increasing, each in [0, d)) with values data[...]; indptr has n+1 entries,
+ * indptr[0] = 0, indptr[n] = nnz.  The support S_i of f_i is the set of
+ * stored entries of row i (reading R3). */
+typedef struct {
+  int64_t n, d, nnz;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const double* data;
+} asaga_csr_view;
+
+typedef struct {
+  int device;            /* CUDA device ordinal (default 0) */
+  int deterministic;     /* 1: a single sample in flight, updates applied in t order; the
+                            iterate then equals sequential Sparse SAGA (tau = 1). Default 0. */
+  int64_t concurrency;   /* async mode: number of samples in flight (the paper's number of
+                            cores p; overlap tau >= p - 1).  0 = auto
+                            (every resident worker of the update kernel). */
+  int lanes_per_sample;  /* lanes of a warp that cooperate on one sample: 8, 16 or 32;
+                            0 = auto from the mean row length */
+  int atomic_mode;       /* 1 (default): red.global.add.f64 coordinate adds (Property 3).
+                            0: plain load + store (lost updates; test-only ablation of
+                            App. E "non-thread safe") */
+  int record_samples;    /* 1: count visits per row (int32[n]) to check the sample stream */
+  void* stream;          /* cudaStream_t to run on (e.g. torch's current stream);
+                            NULL = a stream owned by the context */
+} asaga_options;
+
+typedef struct {
+  int64_t n, d, nnz;
+  double lambda, gamma;
+  double L;               /* max_i ||a_i||^2 / 4 + lambda (reading R7) */
+  int64_t delta_r;        /* max_v n_v (Section 3.4 sparsity measure) */
+  uint64_t t;             /* global update counter: next update uses sample i_t */
+  int64_t concurrency;    /* samples in flight used by the last asaga_run */
+  int lanes_per_sample;
+  int deterministic;
+  int64_t max_row;        /* longest row */
+  int grid, block;        /* launch shape of the update kernel */
+  double last_run_ms;     /* device time of the last blocking asaga_run (CUDA events) */
+} asaga_stats_t;
+
+/* Fill *opt with the defaults listed above. */
+ASAGA_API void asaga_options_default(asaga_options* opt);
+
+/* Copy a HOST CSR matrix and labels y[n] (each +-1) to the device, validate it
+ * (see ASAGA_E_BAD_CSR / _BAD_LABEL), fold labels into the values
+ * (a~_i = b_i a_i, exact), and run the column-frequency pass: n_v, D_v = n/n_v
+ * (0 when n_v = 0), Delta_r, L (Section 2).  State
+ * starts at x = 0, alpha = 0, abar = 0, t = 0 (reading R1).  On success *out
+ * owns all device memory; on failure *out = NULL. */
+ASAGA_API asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y,
+                        double lambda, double gamma, const asaga_options* opt);
+
+/* As asaga_init, but A's three arrays and y are DEVICE pointers (e.g. torch
+ * tensors); they are copied device-to-device and may be freed afterwards.
+ * Validation runs on the device. */
+ASAGA_API asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* A_dev,
+                               const double* y_dev, double lambda, double gamma,
+                               const asaga_options* opt);
+
+/* Re-ingest a new matrix of the SAME shape (n, d, nnz) into an existing
+ * context, reusing its device memory: HOST arrays (asaga_reload) or DEVICE
+ * arrays (asaga_reload_device).  Runs A0-A1 again and resets the state to
+ * x = 0, alpha = 0, abar = 0, t = 0.  Errors as asaga_init; a different shape
+ * gives ASAGA_E_INVALID_ARG.  Blocking (the validation result is read back). */
+ASAGA_API asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y);
+ASAGA_API asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A_dev,
+                                           const double* y_dev);
+
+/* Process the global update counters t = t0 .. t0+n_updates-1 (t0 = the
+ * context's counter, then t0 += n_updates).  Update t uses row
+ * i_t = floor(r_t * n / 2^64), r_t = the first two 32-bit words of
+ * Philox4x32-10(counter = (lo32 t, hi32 t, 0, 0), key = (lo32 seed, hi32 seed))
+ * (reading R2), so run(T1); run(T2) processes the same samples as run(T1+T2),
+ * and in deterministic mode yields the same iterate.  Blocks until done and
+ * then checks x for non-finite values (ASAGA_E_DIVERGED). */
+ASAGA_API asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed);
+
+/* Enqueue the same work on the context's stream and return immediately
+ * (no divergence check, last_run_ms not updated). */
+ASAGA_API asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed);
+
+/* f(x) (Section 4.1 objective, full lambda/2 ||x||^2).  x: HOST d-vector, or NULL
+ * for the current iterate.  Blocking. */
+ASAGA_API asaga_status asaga_objective(asaga_ctx* ctx, const double* x, double* f_out);
+
+/* grad f(x) = (1/n) sum_i sigma_i(x) a_i + lambda x, sigma_i = -b_i/(1+exp(b_i a_i.x))
+ * (gradient of Eq. 1 with the l2 term).  x: HOST d-vector or NULL (current
+ * iterate); g_out: HOST d-vector.  Blocking.  The first call builds a
+ * column-major copy of A on the device (deterministic summation order). */
+ASAGA_API asaga_status asaga_full_grad(asaga_ctx* ctx, const double* x, double* g_out);
+
+/* Enqueue f(x) for DEVICE x (NULL = current iterate) into DEVICE *f_dev. */
+ASAGA_API asaga_status asaga_objective_device(asaga_ctx* ctx, const double* x_dev, double* f_dev);
+
+/* Row-shard partial of the objective/gradient for a context built on a block
+ * of rows: out_dev[0..d) = sum_{i in shard} sigma_i(x) a_i and
+ * out_dev[d] = sum_{i in shard} log(1+exp(-b_i a_i.x)) (no 1/n, no lambda).
+ * x_dev, out_dev: DEVICE pointers; enqueued on `stream` (NULL = context
+ * stream).  Summing the outputs of all shards (an all-reduce) and then
+ * f = out[d]/n + lambda/2 ||x||^2, grad = out[:d]/n + lambda x gives the full
+ * objective and gradient. */
+ASAGA_API asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double* out_dev,
+                                    void* stream);
+
+/* Copy the state to HOST buffers (any may be NULL): x[d], alpha[n] (the
+ * paper's alpha_i, i.e. labels unfolded), alpha_bar[d], t. */
+ASAGA_API asaga_status asaga_get_state(asaga_ctx* ctx, double* x, double* alpha, double* alpha_bar,
+                             uint64_t* t);
+
+/* Overwrite the state from HOST buffers (NULL leaves that part unchanged). */
+ASAGA_API asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alpha,
+                             const double* alpha_bar, const uint64_t* t);
+
+/* Column profile to HOST buffers (either may be NULL): counts[d] = n_v, D[d] = D_v. */
+ASAGA_API asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double* D);
+
+/* Per-row visit counts (HOST int32[n]) since init or the last reset; needs
+ * options.record_samples = 1, else ASAGA_E_STATE. reset != 0 zeroes them after the copy. */
+ASAGA_API asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset);
+
+/* Change the step size gamma (> 0) for subsequent runs. */
+ASAGA_API asaga_status asaga_set_gamma(asaga_ctx* ctx, double gamma);
+
+/* Change the number of samples in flight (async mode; 0 = auto). */
+ASAGA_API asaga_status asaga_set_concurrency(asaga_ctx* ctx, int64_t concurrency);
+
+ASAGA_API asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out);
+
+/* The sampler alone: out_dev[k] = i_{t0+k} for n rows (same map as asaga_run),
+ * DEVICE int64 buffer of `count` entries, enqueued on `stream` (NULL = default
+ * stream of `device`). */
+ASAGA_API asaga_status asaga_sample_indices(int device, uint64_t seed, uint64_t t0, uint64_t count,
+                                  uint64_t n, int64_t* out_dev, void* stream);
+
+/* Device pointer of the context's stream (cudaStream_t). */
+ASAGA_API void* asaga_stream(const asaga_ctx* ctx);
+
+/* Message for the last failure on ctx (or the calling thread's last failure
+ * outside a context when ctx == NULL).  Never NULL; valid until the next call. */
+ASAGA_API const char* asaga_last_error(const asaga_ctx* ctx);
+
+ASAGA_API const char* asaga_status_string(asaga_status s);
+
+ASAGA_API int asaga_abi_version(void);
+
+/* Free all device memory of ctx (NULL-safe). */
+ASAGA_API void asaga_destroy(asaga_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ASAGA_H */

@@ -1,0 +1,829 @@
+// asaga.cu -- the C-ABI of include/asaga.h: context, ingest, launch logic.
+//
+// Every step of the hot path runs in the kernels of asaga_kernels.cuh; this
+// file only validates arguments, owns device memory, picks launch shapes and
+// moves results across the host/device boundary.  The one library primitive
+// used is CUB's radix sort + scan, at init time only, to build the
+// column-major copy the deterministic gradient pass reads.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/asaga.h"
+#include "asaga_kernels.cuh"
+
+using namespace asaga;
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kColSeg = 2048;         // CSC entries per gradient segment
+constexpr int64_t kSmemHistMax = 48 * 1024;  // columns held in a shared histogram
+
+thread_local std::string g_thread_err = "no error";
+
+}  // namespace
+
+struct asaga_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int sms = 148;
+  int64_t n = 0, d = 0, nnz = 0;
+  double lambda = 0, gamma = 0, L = 0;
+  int64_t delta_r = 0, max_row = 0;
+  uint64_t t = 0;
+  int deterministic = 0, atomic_mode = 1, record = 0;
+  int64_t concurrency_opt = 0;
+  int lanes_opt = 0;
+  // device data
+  int64_t* rowptr = nullptr;
+  int32_t* cols = nullptr;
+  double* vals = nullptr;  // folded a~ = b a
+  double* y = nullptr;
+  Coord* st = nullptr;
+  double* alpha = nullptr;  // folded alpha~ = b alpha
+  int32_t* counts = nullptr;
+  int32_t* visits = nullptr;
+  // scratch
+  double* xdense = nullptr;
+  double* sig = nullptr;
+  double* block_loss = nullptr;
+  double* scal = nullptr;  // [0] f, [1] loss sum
+  int* flag = nullptr;
+  unsigned long long* scratch = nullptr;
+  double* tmp_n = nullptr;  // n doubles (state conversions)
+  double* tmp_d = nullptr;  // d doubles
+  double* tmp_d2 = nullptr; // d doubles
+  int obj_blocks = 0;
+  // CSC (built lazily)
+  bool csc_built = false;
+  int32_t* csc_rows = nullptr;
+  double* csc_vals = nullptr;
+  int64_t* seg_ptr = nullptr;
+  int64_t* seg_lo = nullptr;
+  int64_t* seg_hi = nullptr;
+  double* seg_sum = nullptr;
+  int64_t nseg = 0;
+  // update-kernel launch shape
+  int lanes = 32, nr = 1;
+  int overflow = 0;
+  size_t smem = 0;
+  int grid = 1, block = kBlock;
+  int64_t workers = 1;
+  int max_resident_groups = 1;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0.0;
+  std::string err = "no error";
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+asaga_status fail(asaga_ctx* ctx, asaga_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  g_thread_err = buf;
+  return s;
+}
+
+#define CK(ctx, call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      return fail((ctx), e_ == cudaErrorMemoryAllocation ? ASAGA_E_OOM : ASAGA_E_CUDA,    \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,       \
+                  __LINE__);                                                              \
+    }                                                                                     \
+  } while (0)
+
+template <typename T>
+asaga_status dalloc(asaga_ctx* ctx, T** p, size_t count) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+  if (e != cudaSuccess)
+    return fail(ctx, e == cudaErrorMemoryAllocation ? ASAGA_E_OOM : ASAGA_E_CUDA,
+                "cudaMalloc(%zu bytes): %s", count * sizeof(T), cudaGetErrorString(e));
+  ctx->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return ASAGA_OK;
+}
+
+template <typename T>
+void dfree(asaga_ctx* ctx, T** p) {
+  if (!*p) return;
+  auto it = std::find(ctx->allocs.begin(), ctx->allocs.end(), (void*)*p);
+  if (it != ctx->allocs.end()) ctx->allocs.erase(it);
+  cudaFree(*p);
+  *p = nullptr;
+}
+
+#define TRY(expr)                    \
+  do {                               \
+    asaga_status s_ = (expr);        \
+    if (s_ != ASAGA_OK) return s_;   \
+  } while (0)
+
+int grid_for(const asaga_ctx* ctx, int64_t work, int block) {
+  int64_t g = (work + block - 1) / block;
+  int64_t cap = (int64_t)ctx->sms * 8;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+using UpdFn = void (*)(UpdateParams);
+
+template <int G, int NR>
+UpdFn pick_upd(bool det, bool atomic) {
+  if (det) return atomic ? asaga_update_kernel<G, NR, true, true> : asaga_update_kernel<G, NR, true, false>;
+  return atomic ? asaga_update_kernel<G, NR, false, true> : asaga_update_kernel<G, NR, false, false>;
+}
+
+template <int G>
+UpdFn pick_upd_nr(int nr, bool det, bool atomic) {
+  switch (nr) {
+    case 1: return pick_upd<G, 1>(det, atomic);
+    case 2: return pick_upd<G, 2>(det, atomic);
+    case 4: return pick_upd<G, 4>(det, atomic);
+    default: return pick_upd<G, 8>(det, atomic);
+  }
+}
+
+UpdFn update_fn(int lanes, int nr, bool det, bool atomic) {
+  switch (lanes) {
+    case 8: return pick_upd_nr<8>(nr, det, atomic);
+    case 16: return pick_upd_nr<16>(nr, det, atomic);
+    default: return pick_upd_nr<32>(nr, det, atomic);
+  }
+}
+
+// Pick lanes per sample and register chunks from the row-length profile, then
+// the launch shape for the requested number of samples in flight.
+asaga_status configure_update(asaga_ctx* ctx) {
+  const double mean = ctx->n ? (double)ctx->nnz / (double)ctx->n : 1.0;
+  int lanes = ctx->lanes_opt;
+  if (lanes == 0) lanes = mean <= 8.0 ? 8 : (mean <= 16.0 ? 16 : 32);
+  if (lanes != 8 && lanes != 16 && lanes != 32)
+    return fail(ctx, ASAGA_E_INVALID_ARG, "lanes_per_sample must be 0, 8, 16 or 32 (got %d)", lanes);
+  int nr = 1;
+  while (nr < 8 && (double)(nr * lanes) < 2.0 * mean) nr *= 2;
+  if ((int64_t)nr * lanes < ctx->max_row && ctx->max_row <= (int64_t)2 * nr * lanes && nr < 8) nr *= 2;
+  ctx->lanes = lanes;
+  ctx->nr = nr;
+  ctx->overflow = (int)std::max<int64_t>(0, ctx->max_row - (int64_t)nr * lanes);
+  const int groups_per_block = kBlock / lanes;
+  ctx->smem = (size_t)groups_per_block * (size_t)ctx->overflow * sizeof(double);
+  UpdFn fn = update_fn(lanes, nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
+  if (ctx->smem > 227 * 1024)
+    return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
+                (long long)ctx->max_row);
+  CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)ctx->smem));
+  int per_sm = 0;
+  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kBlock, ctx->smem));
+  per_sm = std::max(per_sm, 1);
+  ctx->max_resident_groups = per_sm * ctx->sms * groups_per_block;
+  int64_t workers;
+  if (ctx->deterministic) workers = 1;
+  else if (ctx->concurrency_opt > 0) workers = std::min<int64_t>(ctx->concurrency_opt, ctx->max_resident_groups);
+  else workers = ctx->max_resident_groups;
+  ctx->workers = workers;
+  ctx->block = kBlock;
+  ctx->grid = (int)((workers + groups_per_block - 1) / groups_per_block);
+  return ASAGA_OK;
+}
+
+// Device buffers of a context (sizes fixed by n, d, nnz).
+asaga_status alloc_state(asaga_ctx* ctx) {
+  const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
+  TRY(dalloc(ctx, &ctx->rowptr, n + 1));
+  TRY(dalloc(ctx, &ctx->cols, nnz));
+  TRY(dalloc(ctx, &ctx->y, n));
+  TRY(dalloc(ctx, &ctx->vals, nnz));
+  TRY(dalloc(ctx, &ctx->st, d));
+  TRY(dalloc(ctx, &ctx->alpha, n));
+  TRY(dalloc(ctx, &ctx->counts, d));
+  TRY(dalloc(ctx, &ctx->xdense, d));
+  TRY(dalloc(ctx, &ctx->tmp_n, n));
+  TRY(dalloc(ctx, &ctx->tmp_d, d));
+  TRY(dalloc(ctx, &ctx->tmp_d2, d));
+  ctx->obj_blocks = ctx->sms * 4;
+  TRY(dalloc(ctx, &ctx->block_loss, ctx->obj_blocks));
+  TRY(dalloc(ctx, &ctx->scal, 4));
+  TRY(dalloc(ctx, &ctx->flag, 4));
+  TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 2));  // err rows, max ||a||^2, max row
+  if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
+  return ASAGA_OK;
+}
+
+// A0 + A1 on data already in device memory: rowptr/cols/y in the context's own
+// buffers, values in data_in (the caller's device array, or ctx->vals itself
+// after a host copy -- the fold is elementwise, so in place is safe).  Resets
+// the state to x = 0, alpha = 0, abar = 0, t = 0 (reading R1).
+asaga_status ingest(asaga_ctx* ctx, const double* data_in) {
+  const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
+  unsigned long long* scratch = ctx->scratch;
+  if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
+  CK(ctx, cudaMemsetAsync(ctx->counts, 0, sizeof(int32_t) * d, ctx->stream));
+  CK(ctx, cudaMemsetAsync(ctx->alpha, 0, sizeof(double) * n, ctx->stream));
+  CK(ctx, cudaMemsetAsync(scratch, 0xff, sizeof(unsigned long long) * ERR_COUNT, ctx->stream));
+  CK(ctx, cudaMemsetAsync(scratch + ERR_COUNT, 0, sizeof(unsigned long long) * 2, ctx->stream));
+  CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
+  ctx->t = 0;
+  if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    dfree(ctx, &ctx->csc_rows);
+    dfree(ctx, &ctx->csc_vals);
+    dfree(ctx, &ctx->seg_ptr);
+    dfree(ctx, &ctx->seg_lo);
+    dfree(ctx, &ctx->seg_hi);
+    dfree(ctx, &ctx->seg_sum);
+    dfree(ctx, &ctx->sig);
+    ctx->csc_built = false;
+  }
+
+  IngestParams ip;
+  ip.indptr = ctx->rowptr;
+  ip.indices = ctx->cols;
+  ip.data = data_in;
+  ip.y = ctx->y;
+  ip.vals = ctx->vals;
+  ip.counts = ctx->counts;
+  ip.err_row = scratch;
+  ip.max_sq = scratch + ERR_COUNT;
+  ip.max_len = scratch + ERR_COUNT + 1;
+  ip.n = n;
+  ip.d = d;
+  ip.nnz = nnz;
+  ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
+  const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 0;
+  CK(ctx, cudaFuncSetAttribute((const void*)ingest_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
+  int per_sm = 1;
+  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ingest_kernel, kBlock, hsmem));
+  per_sm = std::max(per_sm, 1);
+  int64_t want = (n + (kBlock / 32) - 1) / (kBlock / 32);
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
+  ingest_kernel<<<grid, kBlock, hsmem, ctx->stream>>>(ip);
+  CK(ctx, cudaGetLastError());
+  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->st, d, n,
+                                                                        ctx->flag + 1);
+  CK(ctx, cudaGetLastError());
+  unsigned long long h[ERR_COUNT + 2];
+  int hmax_count = 0;
+  CK(ctx, cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(&hmax_count, ctx->flag + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
+  static const char* what[ERR_COUNT] = {"row pointers out of order or out of [0, nnz]",
+                                        "empty row (rows must be non-empty)",
+                                        "column index out of [0, d)",
+                                        "column indices not strictly increasing",
+                                        "non-finite value",
+                                        "label not in {-1, +1}"};
+  for (int e = 0; e < ERR_COUNT; ++e) {
+    if (h[e] != ULLONG_MAX) {
+      asaga_status s = e == ERR_LABEL ? ASAGA_E_BAD_LABEL : ASAGA_E_BAD_CSR;
+      return fail(ctx, s, "row %llu: %s", h[e], what[e]);
+    }
+  }
+  double max_sq;
+  std::memcpy(&max_sq, &h[ERR_COUNT], sizeof(double));
+  ctx->L = max_sq / 4.0 + ctx->lambda;
+  ctx->max_row = (int64_t)h[ERR_COUNT + 1];
+  ctx->delta_r = hmax_count;
+  return configure_update(ctx);
+}
+
+asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
+                      double gamma, const asaga_options* opt, asaga_ctx** ctx_out) {
+  if (!out) return fail(nullptr, ASAGA_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!A || !y) return fail(nullptr, ASAGA_E_INVALID_ARG, "A or y is NULL");
+  if (!A->indptr || (A->nnz > 0 && (!A->indices || !A->data)))
+    return fail(nullptr, ASAGA_E_INVALID_ARG, "CSR arrays are NULL");
+  if (A->n <= 0 || A->d <= 0 || A->nnz < 0)
+    return fail(nullptr, ASAGA_E_INVALID_ARG, "need n > 0, d > 0, nnz >= 0 (n=%lld d=%lld nnz=%lld)",
+                (long long)A->n, (long long)A->d, (long long)A->nnz);
+  if (A->d > INT32_MAX) return fail(nullptr, ASAGA_E_INVALID_ARG, "d exceeds int32 indices");
+  if (!(lambda > 0.0) || !std::isfinite(lambda))
+    return fail(nullptr, ASAGA_E_INVALID_ARG, "lambda must be > 0 (got %g)", lambda);
+  if (!(gamma > 0.0) || !std::isfinite(gamma))
+    return fail(nullptr, ASAGA_E_INVALID_ARG, "gamma must be > 0 (got %g)", gamma);
+  asaga_options o;
+  asaga_options_default(&o);
+  if (opt) o = *opt;
+  asaga_ctx* ctx = new asaga_ctx();
+  ctx->device = o.device;
+  ctx->n = A->n;
+  ctx->d = A->d;
+  ctx->nnz = A->nnz;
+  ctx->lambda = lambda;
+  ctx->gamma = gamma;
+  ctx->deterministic = o.deterministic ? 1 : 0;
+  ctx->atomic_mode = o.atomic_mode ? 1 : 0;
+  ctx->record = o.record_samples ? 1 : 0;
+  ctx->concurrency_opt = o.concurrency;
+  ctx->lanes_opt = o.lanes_per_sample;
+  *ctx_out = ctx;
+  cudaError_t e = cudaSetDevice(o.device);
+  if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
+  CK(ctx, cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, o.device));
+  if (o.stream) {
+    ctx->stream = (cudaStream_t)o.stream;
+  } else {
+    CK(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CK(ctx, cudaEventCreate(&ctx->ev0));
+  CK(ctx, cudaEventCreate(&ctx->ev1));
+  return ASAGA_OK;
+}
+
+asaga_status finish_init(asaga_ctx** out, asaga_ctx* ctx, asaga_status s) {
+  if (s != ASAGA_OK) {
+    if (ctx) {
+      g_thread_err = ctx->err;
+      asaga_destroy(ctx);
+    }
+    *out = nullptr;
+    return s;
+  }
+  *out = ctx;
+  return ASAGA_OK;
+}
+
+asaga_status ensure_csc(asaga_ctx* ctx) {
+  if (ctx->csc_built) return ASAGA_OK;
+  const int64_t d = ctx->d, nnz = ctx->nnz, n = ctx->n;
+  cudaStream_t s = ctx->stream;
+  int64_t *colptr = nullptr, *cnt64 = nullptr, *perm_in = nullptr, *perm_out = nullptr;
+  int32_t *keys_out = nullptr, *row_of = nullptr;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    for (void* p : {(void*)colptr, (void*)cnt64, (void*)perm_in, (void*)perm_out, (void*)keys_out,
+                    (void*)row_of})
+      if (p) cudaFree(p);
+  };
+#define CKC(call)                                                                           \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      cleanup();                                                                            \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? ASAGA_E_OOM : ASAGA_E_CUDA,        \
+                  "%s failed: %s", #call, cudaGetErrorString(e_));                          \
+    }                                                                                       \
+  } while (0)
+  CKC(cudaMalloc(&colptr, sizeof(int64_t) * (d + 1)));
+  CKC(cudaMalloc(&cnt64, sizeof(int64_t) * (d + 1)));
+  CKC(cudaMalloc(&perm_in, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+  CKC(cudaMalloc(&perm_out, sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+  CKC(cudaMalloc(&keys_out, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  CKC(cudaMalloc(&row_of, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  // colptr = exclusive scan of n_v
+  CKC(cudaMemsetAsync(cnt64, 0, sizeof(int64_t) * (d + 1), s));
+  segcount_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, s>>>(ctx->counts, d, 1, cnt64);
+  CKC(cudaGetLastError());
+  size_t tb = 0, tb2 = 0;
+  CKC(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt64, colptr, d + 1, s));
+  int end_bit = 1;
+  while (end_bit < 31 && (int64_t(1) << end_bit) < d) ++end_bit;
+  CKC(cub::DeviceRadixSort::SortPairs(nullptr, tb2, ctx->cols, keys_out, perm_in, perm_out, nnz, 0,
+                                      end_bit, s));
+  void* temp = nullptr;
+  CKC(cudaMalloc(&temp, std::max(tb, tb2)));
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb, cnt64, colptr, d + 1, s);
+  if (e == cudaSuccess) {
+    iota_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, s>>>(perm_in, nnz);
+    e = cub::DeviceRadixSort::SortPairs(temp, tb2, ctx->cols, keys_out, perm_in, perm_out, nnz, 0,
+                                        end_bit, s);
+  }
+  cudaStreamSynchronize(s);
+  cudaFree(temp);
+  CKC(e);
+  asaga_status st;
+  if ((st = dalloc(ctx, &ctx->csc_rows, nnz)) != ASAGA_OK) { cleanup(); return st; }
+  if ((st = dalloc(ctx, &ctx->csc_vals, nnz)) != ASAGA_OK) { cleanup(); return st; }
+  row_of_kernel<<<grid_for(ctx, n * 32, kBlock), kBlock, 0, s>>>(ctx->rowptr, n, row_of);
+  csc_gather_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, s>>>(perm_out, row_of, ctx->vals, nnz,
+                                                                    ctx->csc_rows, ctx->csc_vals);
+  CKC(cudaGetLastError());
+  // fixed segments of <= kColSeg entries per column (deterministic summation order)
+  if ((st = dalloc(ctx, &ctx->seg_ptr, d + 1)) != ASAGA_OK) { cleanup(); return st; }
+  CKC(cudaMemsetAsync(cnt64, 0, sizeof(int64_t) * (d + 1), s));
+  segcount_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, s>>>(ctx->counts, d, kColSeg, cnt64);
+  CKC(cudaMalloc(&temp, tb));
+  e = cub::DeviceScan::ExclusiveSum(temp, tb, cnt64, ctx->seg_ptr, d + 1, s);
+  cudaStreamSynchronize(s);
+  cudaFree(temp);
+  CKC(e);
+  CKC(cudaMemcpy(&ctx->nseg, ctx->seg_ptr + d, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if ((st = dalloc(ctx, &ctx->seg_lo, ctx->nseg)) != ASAGA_OK) { cleanup(); return st; }
+  if ((st = dalloc(ctx, &ctx->seg_hi, ctx->nseg)) != ASAGA_OK) { cleanup(); return st; }
+  if ((st = dalloc(ctx, &ctx->seg_sum, ctx->nseg)) != ASAGA_OK) { cleanup(); return st; }
+  if ((st = dalloc(ctx, &ctx->sig, n)) != ASAGA_OK) { cleanup(); return st; }
+  segfill_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, s>>>(colptr, ctx->seg_ptr, d, kColSeg,
+                                                             ctx->seg_lo, ctx->seg_hi);
+  CKC(cudaGetLastError());
+  cleanup();
+#undef CKC
+  ctx->csc_built = true;
+  return ASAGA_OK;
+}
+
+// Enqueue margins (+ sigma~ if want_sig) and the objective finish for device x.
+asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, double* f_dev,
+                               double* loss_sum_dev, bool want_sig, cudaStream_t s) {
+  const double mean = (double)ctx->nnz / (double)ctx->n;
+  double* sig = want_sig ? ctx->sig : nullptr;
+  if (mean <= 8.0)
+    margin_kernel<8><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+                                                        ctx->n, sig, ctx->block_loss);
+  else if (mean <= 16.0)
+    margin_kernel<16><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+                                                         ctx->n, sig, ctx->block_loss);
+  else
+    margin_kernel<32><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+                                                         ctx->n, sig, ctx->block_loss);
+  CK(ctx, cudaGetLastError());
+  finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, ctx->d,
+                                             ctx->n, ctx->lambda, f_dev, loss_sum_dev);
+  CK(ctx, cudaGetLastError());
+  return ASAGA_OK;
+}
+
+// Enqueue sum_i sigma~_i a~_i (raw, divide=0) or the full gradient (divide=1) into g_dev.
+asaga_status enqueue_gradient(asaga_ctx* ctx, const double* x_dev, double* g_dev, int divide,
+                              cudaStream_t s) {
+  colseg_kernel<<<grid_for(ctx, ctx->nseg * 32, kBlock), kBlock, 0, s>>>(
+      ctx->seg_lo, ctx->seg_hi, ctx->nseg, ctx->csc_rows, ctx->csc_vals, ctx->sig, ctx->seg_sum);
+  CK(ctx, cudaGetLastError());
+  colsum_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
+      ctx->seg_ptr, ctx->seg_sum, x_dev, ctx->d, (double)ctx->n, ctx->lambda, g_dev, divide);
+  CK(ctx, cudaGetLastError());
+  return ASAGA_OK;
+}
+
+const double* current_x(asaga_ctx* ctx, cudaStream_t s) {
+  extract_x_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->st, ctx->xdense, ctx->d);
+  return ctx->xdense;
+}
+
+asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool timed) {
+  if (n_updates == 0) return ASAGA_OK;
+  UpdateParams p;
+  p.rowptr = ctx->rowptr;
+  p.cols = ctx->cols;
+  p.vals = ctx->vals;
+  p.st = ctx->st;
+  p.alpha = ctx->alpha;
+  p.visits = ctx->visits;
+  p.n = (uint64_t)ctx->n;
+  p.gamma = ctx->gamma;
+  p.lambda_ = ctx->lambda;
+  p.inv_n = 1.0 / (double)ctx->n;
+  p.seed = seed;
+  p.t0 = ctx->t;
+  p.T = n_updates;
+  p.workers = ctx->workers;
+  p.overflow = ctx->overflow;
+  UpdFn fn = update_fn(ctx->lanes, ctx->nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
+  // Fewer updates than workers: launch only what is needed.
+  int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
+  p.workers = ctx->workers;  // the stride stays W so the t -> worker map is launch-independent
+  const int gpb = kBlock / ctx->lanes;
+  int grid = (int)((workers + gpb - 1) / gpb);
+  if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+  void* args[] = {&p};
+  CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(kBlock), args, ctx->smem, ctx->stream));
+  if (timed) CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->t += n_updates;
+  return ASAGA_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+void asaga_options_default(asaga_options* opt) {
+  if (!opt) return;
+  opt->device = 0;
+  opt->deterministic = 0;
+  opt->concurrency = 0;
+  opt->lanes_per_sample = 0;
+  opt->atomic_mode = 1;
+  opt->record_samples = 0;
+  opt->stream = nullptr;
+}
+
+asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
+                        double gamma, const asaga_options* opt) {
+  asaga_ctx* ctx = nullptr;
+  asaga_status s = make_ctx(out, A, y, lambda, gamma, opt, &ctx);
+  if (s != ASAGA_OK) return finish_init(out, ctx, s);
+  s = alloc_state(ctx);
+  if (s == ASAGA_OK) s = asaga_reload(ctx, A, y);
+  return finish_init(out, ctx, s);
+}
+
+asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* A, const double* y,
+                               double lambda, double gamma, const asaga_options* opt) {
+  asaga_ctx* ctx = nullptr;
+  asaga_status s = make_ctx(out, A, y, lambda, gamma, opt, &ctx);
+  if (s != ASAGA_OK) return finish_init(out, ctx, s);
+  s = alloc_state(ctx);
+  if (s == ASAGA_OK) s = asaga_reload_device(ctx, A, y);
+  return finish_init(out, ctx, s);
+}
+
+static asaga_status check_same_shape(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  if (!A || !y || !A->indptr || (A->nnz > 0 && (!A->indices || !A->data)))
+    return fail(ctx, ASAGA_E_INVALID_ARG, "NULL CSR array or labels");
+  if (A->n != ctx->n || A->d != ctx->d || A->nnz != ctx->nnz)
+    return fail(ctx, ASAGA_E_INVALID_ARG, "reload needs the context's shape (n=%lld d=%lld nnz=%lld)",
+                (long long)ctx->n, (long long)ctx->d, (long long)ctx->nnz);
+  return ASAGA_OK;
+}
+
+asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
+  TRY(check_same_shape(ctx, A, y));
+  CK(ctx, cudaSetDevice(ctx->device));
+  if (A->indptr[0] != 0 || A->indptr[A->n] != A->nnz)
+    return fail(ctx, ASAGA_E_BAD_CSR, "indptr[0] must be 0 and indptr[n] must be nnz (got %lld and %lld, nnz=%lld)",
+                (long long)A->indptr[0], (long long)A->indptr[A->n], (long long)A->nnz);
+  // host -> device: the host/device boundary.  Values land in ctx->vals and are
+  // folded in place by the ingest kernel.
+  CK(ctx, cudaMemcpyAsync(ctx->rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->vals, A->data, sizeof(double) * ctx->nnz, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->y, y, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+  return ingest(ctx, ctx->vals);
+}
+
+asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
+  TRY(check_same_shape(ctx, A, y));
+  CK(ctx, cudaSetDevice(ctx->device));
+  int64_t ends[2];
+  CK(ctx, cudaMemcpyAsync(&ends[0], A->indptr, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(&ends[1], A->indptr + ctx->n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ends[0] != 0 || ends[1] != ctx->nnz)
+    return fail(ctx, ASAGA_E_BAD_CSR, "indptr[0] must be 0 and indptr[n] must be nnz (got %lld and %lld, nnz=%lld)",
+                (long long)ends[0], (long long)ends[1], (long long)ctx->nnz);
+  CK(ctx, cudaMemcpyAsync(ctx->rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1),
+                          cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->y, y, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+  return ingest(ctx, A->data);
+}
+
+asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  return enqueue_run(ctx, n_updates, seed, false);
+}
+
+asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  if (n_updates == 0) return ASAGA_OK;
+  TRY(enqueue_run(ctx, n_updates, seed, true));
+  CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
+  nonfinite_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->st, ctx->d, ctx->flag);
+  CK(ctx, cudaGetLastError());
+  int bad = 0;
+  CK(ctx, cudaMemcpyAsync(&bad, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  CK(ctx, cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  ctx->last_ms = ms;
+  if (bad) return fail(ctx, ASAGA_E_DIVERGED, "non-finite iterate after %llu updates (gamma=%g too large?)",
+                       (unsigned long long)ctx->t, ctx->gamma);
+  return ASAGA_OK;
+}
+
+asaga_status asaga_objective_device(asaga_ctx* ctx, const double* x_dev, double* f_dev) {
+  if (!ctx || !f_dev) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_dev is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  const double* x = x_dev ? x_dev : current_x(ctx, ctx->stream);
+  return enqueue_objective(ctx, x, f_dev, nullptr, false, ctx->stream);
+}
+
+asaga_status asaga_objective(asaga_ctx* ctx, const double* x, double* f_out) {
+  if (!ctx || !f_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_out is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  const double* xd;
+  if (x) {
+    CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, ctx->stream));
+    xd = ctx->tmp_d;
+  } else {
+    xd = current_x(ctx, ctx->stream);
+  }
+  TRY(enqueue_objective(ctx, xd, ctx->scal, nullptr, false, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(f_out, ctx->scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_full_grad(asaga_ctx* ctx, const double* x, double* g_out) {
+  if (!ctx || !g_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or g_out is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(ensure_csc(ctx));
+  const double* xd;
+  if (x) {
+    CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, ctx->stream));
+    xd = ctx->tmp_d;
+  } else {
+    xd = current_x(ctx, ctx->stream);
+  }
+  TRY(enqueue_objective(ctx, xd, ctx->scal, nullptr, true, ctx->stream));
+  TRY(enqueue_gradient(ctx, xd, ctx->tmp_d2, 1, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(g_out, ctx->tmp_d2, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double* out_dev, void* stream) {
+  if (!ctx || !x_dev || !out_dev) return fail(ctx, ASAGA_E_INVALID_ARG, "NULL argument");
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(ensure_csc(ctx));
+  cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  TRY(enqueue_objective(ctx, x_dev, nullptr, out_dev + ctx->d, true, s));
+  TRY(enqueue_gradient(ctx, x_dev, out_dev, 0, s));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_get_state(asaga_ctx* ctx, double* x, double* alpha, double* alpha_bar, uint64_t* t) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (x || alpha_bar) {
+    unpack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
+        ctx->st, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, nullptr, ctx->d);
+    CK(ctx, cudaGetLastError());
+    if (x) CK(ctx, cudaMemcpyAsync(x, ctx->tmp_d, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
+    if (alpha_bar)
+      CK(ctx, cudaMemcpyAsync(alpha_bar, ctx->tmp_d2, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
+  }
+  if (alpha) {
+    fold_alpha_kernel<<<grid_for(ctx, ctx->n, kBlock), kBlock, 0, s>>>(ctx->alpha, ctx->y, ctx->tmp_n, ctx->n);
+    CK(ctx, cudaGetLastError());
+    CK(ctx, cudaMemcpyAsync(alpha, ctx->tmp_n, sizeof(double) * ctx->n, cudaMemcpyDeviceToHost, s));
+  }
+  CK(ctx, cudaStreamSynchronize(s));
+  if (t) *t = ctx->t;
+  return ASAGA_OK;
+}
+
+asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alpha,
+                             const double* alpha_bar, const uint64_t* t) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (x) CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
+  if (alpha_bar)
+    CK(ctx, cudaMemcpyAsync(ctx->tmp_d2, alpha_bar, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
+  if (x || alpha_bar) {
+    pack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
+        ctx->st, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
+    CK(ctx, cudaGetLastError());
+  }
+  if (alpha) {
+    CK(ctx, cudaMemcpyAsync(ctx->tmp_n, alpha, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, s));
+    fold_alpha_kernel<<<grid_for(ctx, ctx->n, kBlock), kBlock, 0, s>>>(ctx->tmp_n, ctx->y, ctx->alpha, ctx->n);
+    CK(ctx, cudaGetLastError());
+  }
+  CK(ctx, cudaStreamSynchronize(s));
+  if (t) ctx->t = *t;
+  return ASAGA_OK;
+}
+
+asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double* D) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  CK(ctx, cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (counts)
+    CK(ctx, cudaMemcpyAsync(counts, ctx->counts, sizeof(int32_t) * ctx->d, cudaMemcpyDeviceToHost, s));
+  if (D) {
+    unpack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->st, nullptr, nullptr,
+                                                                         ctx->tmp_d, ctx->d);
+    CK(ctx, cudaGetLastError());
+    CK(ctx, cudaMemcpyAsync(D, ctx->tmp_d, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
+  }
+  CK(ctx, cudaStreamSynchronize(s));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset) {
+  if (!ctx || !visits) return fail(ctx, ASAGA_E_INVALID_ARG, "NULL argument");
+  if (!ctx->visits) return fail(ctx, ASAGA_E_STATE, "context was created without record_samples");
+  CK(ctx, cudaSetDevice(ctx->device));
+  CK(ctx, cudaMemcpyAsync(visits, ctx->visits, sizeof(int32_t) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (reset) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * ctx->n, ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_set_gamma(asaga_ctx* ctx, double gamma) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  if (!(gamma > 0.0) || !std::isfinite(gamma))
+    return fail(ctx, ASAGA_E_INVALID_ARG, "gamma must be > 0 (got %g)", gamma);
+  ctx->gamma = gamma;
+  return ASAGA_OK;
+}
+
+asaga_status asaga_set_concurrency(asaga_ctx* ctx, int64_t concurrency) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  if (concurrency < 0) return fail(ctx, ASAGA_E_INVALID_ARG, "concurrency must be >= 0");
+  if (ctx->deterministic) return fail(ctx, ASAGA_E_STATE, "deterministic context has concurrency 1");
+  CK(ctx, cudaSetDevice(ctx->device));
+  ctx->concurrency_opt = concurrency;
+  return configure_update(ctx);
+}
+
+asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
+  if (!ctx || !out) return fail(nullptr, ASAGA_E_INVALID_ARG, "NULL argument");
+  out->n = ctx->n;
+  out->d = ctx->d;
+  out->nnz = ctx->nnz;
+  out->lambda = ctx->lambda;
+  out->gamma = ctx->gamma;
+  out->L = ctx->L;
+  out->delta_r = ctx->delta_r;
+  out->t = ctx->t;
+  out->concurrency = ctx->workers;
+  out->lanes_per_sample = ctx->lanes;
+  out->deterministic = ctx->deterministic;
+  out->max_row = ctx->max_row;
+  out->grid = ctx->grid;
+  out->block = ctx->block;
+  out->last_run_ms = ctx->last_ms;
+  return ASAGA_OK;
+}
+
+asaga_status asaga_sample_indices(int device, uint64_t seed, uint64_t t0, uint64_t count, uint64_t n,
+                                  int64_t* out_dev, void* stream) {
+  if (!out_dev || n == 0) return fail(nullptr, ASAGA_E_INVALID_ARG, "out_dev NULL or n == 0");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, ASAGA_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  if (count == 0) return ASAGA_OK;
+  int grid = (int)std::min<uint64_t>((count + kBlock - 1) / kBlock, 148 * 16);
+  sample_kernel<<<grid, kBlock, 0, (cudaStream_t)stream>>>(seed, t0, count, n, out_dev);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(nullptr, ASAGA_E_CUDA, "sample_kernel: %s", cudaGetErrorString(e));
+  return ASAGA_OK;
+}
+
+void* asaga_stream(const asaga_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+const char* asaga_last_error(const asaga_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_thread_err.c_str();
+}
+
+const char* asaga_status_string(asaga_status s) {
+  switch (s) {
+    case ASAGA_OK: return "ASAGA_OK";
+    case ASAGA_E_INVALID_ARG: return "ASAGA_E_INVALID_ARG";
+    case ASAGA_E_BAD_CSR: return "ASAGA_E_BAD_CSR";
+    case ASAGA_E_BAD_LABEL: return "ASAGA_E_BAD_LABEL";
+    case ASAGA_E_CUDA: return "ASAGA_E_CUDA";
+    case ASAGA_E_OOM: return "ASAGA_E_OOM";
+    case ASAGA_E_DIVERGED: return "ASAGA_E_DIVERGED";
+    case ASAGA_E_STATE: return "ASAGA_E_STATE";
+  }
+  return "ASAGA_E_UNKNOWN";
+}
+
+int asaga_abi_version(void) { return ASAGA_ABI_VERSION; }
+
+void asaga_destroy(asaga_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+}  // extern "C"

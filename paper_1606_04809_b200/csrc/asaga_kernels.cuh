@@ -1,0 +1,529 @@
+// asaga_kernels.cuh -- sm_100a device code of the ASAGA hot path.
+//
+// Paper: Leblond, Pedregosa, Lacoste-Julien, "ASAGA: Asynchronous Parallel
+// SAGA", arXiv 1606.04809 (PAPER.md; cited "P:<line>").  Kernel map
+// (DESIGN.md "Kernels"):
+//   ingest_kernel        A0+A1: validate CSR, fold labels (a~ = b a), n_v, ||a_i||^2
+//   profile_kernel       A1: D_v = n/n_v, coordinate state {x, abar, D} init, Delta_r
+//   asaga_update_kernel  A2..A8: Philox sample -> row -> gather-dot -> sigma -> SAGA
+//                        correction -> red.global.add.f64 scatter (Alg. 2)
+//   margin_kernel        A9: m_i = a~_i.x, softplus(-m_i), sigma~_i (Section 4.1)
+//   colseg_kernel        A9: sum_i sigma~_i a~_iv over fixed column segments (CSC)
+// No tensor cores: nothing here is a dense contraction.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace asaga {
+
+// Coordinate state, one 32-byte sector per feature v: the three values an
+// update gathers for v (x_v, abar_v, D_v) arrive in ONE 256-bit L2 load.
+struct __align__(32) Coord {
+  double x;     // iterate x_v
+  double abar;  // maintained abar_v = (1/n) sum_i alpha_i a_iv
+  double D;     // reweighting D_v = 1/p_v = n / n_v; 0 if n_v = 0
+  double pad;
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11) -- own implementation (the oracle has its
+// own; pin P1 checks both against cuRAND).  Sampling before any read: P:265.
+__device__ __forceinline__ uint2 philox_lo64(uint64_t t, uint64_t seed) {
+  uint32_t c0 = (uint32_t)t, c1 = (uint32_t)(t >> 32), c2 = 0u, c3 = 0u;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+  return make_uint2(c0, c1);
+}
+
+// i_t = floor(r * n / 2^64), r = (w1 << 32) | w0 (reading R2).
+__device__ __forceinline__ int64_t sample_row(uint64_t seed, uint64_t t, uint64_t n) {
+  const uint2 w = philox_lo64(t, seed);
+  const uint64_t r = ((uint64_t)w.y << 32) | (uint64_t)w.x;
+  return (int64_t)__umul64hi(r, n);
+}
+
+// ---------------------------------------------------------------------------
+// Memory-access helpers.  Shared state (Coord, alpha) is read with .cg
+// (LDG.STRONG.GPU: L1 bypass), so a read never returns a stale L1 line of a
+// coordinate another SM has since added to -- the paper's "inconsistent read"
+// is still unsynchronised, but bounded by in-flight updates.
+__device__ __forceinline__ void ld_coord(const Coord* p, double& x, double& ab, double& D) {
+  double pad;
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(x), "=d"(ab), "=d"(D), "=d"(pad)
+               : "l"(p));
+  (void)pad;
+}
+__device__ __forceinline__ double ld_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_cg(double* p, double v) {
+  asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+// Atomic coordinate add (Property 3): fire-and-forget reduction at L2.
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ int ld_nc_i32(const int32_t* p) { return __ldg(p); }
+__device__ __forceinline__ double ld_nc_f64(const double* p) { return __ldg(p); }
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v, unsigned mask) {
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(mask, v, off);
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// A0 + A1: validation, label folding, column counts, squared row norms.
+enum : int { ERR_ROW_BOUNDS = 0, ERR_EMPTY_ROW, ERR_INDEX_RANGE, ERR_INDEX_ORDER,
+             ERR_NONFINITE, ERR_LABEL, ERR_COUNT };
+
+struct IngestParams {
+  const int64_t* indptr;  // n+1
+  const int32_t* indices; // nnz
+  const double* data;     // nnz (unfolded)
+  const double* y;        // n
+  double* vals;           // out: folded values b_i a_ik
+  int32_t* counts;        // out (pre-zeroed): n_v
+  unsigned long long* err_row;   // [ERR_COUNT], pre-set to ULLONG_MAX; atomicMin(row)
+  unsigned long long* max_sq;    // bits of max_i ||a_i||^2 (>= 0 doubles order as u64)
+  unsigned long long* max_len;   // longest row
+  int64_t n, d, nnz;
+  int smem_hist;          // 1: per-block shared histogram of all d columns
+};
+
+__global__ void __launch_bounds__(256) ingest_kernel(IngestParams p) {
+  extern __shared__ int32_t hist[];
+  __shared__ double warp_max[8];
+  __shared__ long long warp_len[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (p.smem_hist) {
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
+    __syncthreads();
+  }
+  double my_max = 0.0;
+  int64_t my_len = 0;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < p.n; i += warps) {
+    const int64_t lo = p.indptr[i], hi = p.indptr[i + 1];
+    if (lo < 0 || hi > p.nnz || hi < lo) {
+      if (lane == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
+      continue;
+    }
+    if (hi == lo) {
+      if (lane == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
+      continue;
+    }
+    my_len = max(my_len, hi - lo);
+    const double b = p.y[i];
+    if (b != 1.0 && b != -1.0) {
+      if (lane == 0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
+    }
+    double sq = 0.0;
+    bool bad_range = false, bad_order = false, bad_val = false;
+    for (int64_t k = lo + lane; k < hi; k += 32) {
+      const int32_t c = p.indices[k];
+      const double v = p.data[k];
+      bad_range |= (c < 0) || ((int64_t)c >= p.d);
+      if (k > lo) bad_order |= (p.indices[k - 1] >= c);
+      bad_val |= !isfinite(v);
+      p.vals[k] = b * v;
+      sq = fma(v, v, sq);
+      if (c >= 0 && (int64_t)c < p.d) {
+        if (p.smem_hist) atomicAdd(&hist[c], 1);
+        else atomicAdd(&p.counts[c], 1);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad_range) && lane == 0)
+      atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+    if (__any_sync(0xffffffffu, bad_order) && lane == 0)
+      atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+    if (__any_sync(0xffffffffu, bad_val) && lane == 0)
+      atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+    sq = group_sum<32>(sq, 0xffffffffu);
+    my_max = fmax(my_max, sq);
+  }
+  if (lane == 0) {
+    warp_max[wib] = my_max;
+    warp_len[wib] = my_len;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    long long L = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      m = fmax(m, warp_max[w]);
+      L = max(L, warp_len[w]);
+    }
+    atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
+    atomicMax(p.max_len, (unsigned long long)L);
+  }
+  if (p.smem_hist) {
+    __syncthreads();
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
+      if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
+  }
+}
+
+// A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
+__global__ void profile_kernel(const int32_t* __restrict__ counts, Coord* __restrict__ st,
+                               int64_t d, int64_t n, int* __restrict__ max_count) {
+  int my = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int c = counts[v];
+    Coord s;
+    s.x = 0.0;
+    s.abar = 0.0;
+    s.D = c > 0 ? (double)n / (double)c : 0.0;
+    s.pad = 0.0;
+    st[v] = s;
+    my = max(my, c);
+  }
+  for (int off = 16; off > 0; off >>= 1) my = max(my, __shfl_xor_sync(0xffffffffu, my, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(max_count, my);
+}
+
+// ---------------------------------------------------------------------------
+// A2..A8: the ASAGA update loop (Algorithm 2, + Section 4.2 l2 term).
+//
+// Worker w (a group of G lanes) processes t = t0 + w, t0 + w + W, ... (W workers
+// = samples in flight).  Per sample, with folded values a~ = b a and folded
+// memory alpha~_i = b_i alpha_i (exact: b = +-1):
+//   i      = Philox(seed, t)                               line 3 (sample first)
+//   x^, abar^ on S_i via one 256-bit .cg load per v        lines 5, 7
+//   m      = sum a~_k x^_{c_k}   (group shuffle reduce)
+//   dalpha = -1/(1+exp(m)) - alpha~^_i                     lines 6, 8
+//   x_v   += -gamma (dalpha a~_k + D_v (abar^_v + lambda x^_v))   line 9, 11
+//   abar_v += dalpha a~_k / n                              line 13
+//   alpha~_i += dalpha                                     line 12 (reading R9)
+// The first NR*G entries of a row keep (c, a~, q = D(abar + lambda x)) in
+// registers; longer rows stash q in shared memory and re-read c, a~ (read-only).
+// DET: one worker; a gpu-scope fence + __syncwarp between samples makes sample
+// t+1 read every write of sample t, i.e. sequential Sparse SAGA.
+struct UpdateParams {
+  const int64_t* rowptr;
+  const int32_t* cols;
+  const double* vals;   // folded a~
+  Coord* st;
+  double* alpha;        // folded alpha~
+  int32_t* visits;      // NULL unless record_samples
+  uint64_t n;
+  double gamma, lambda_, inv_n;
+  uint64_t seed, t0, T;
+  int64_t workers;
+  int overflow;         // shared-memory q slots per group (>= max_row - NR*G, or 0)
+};
+
+template <int G, int NR, bool DET, bool ATOMIC>
+__global__ void __launch_bounds__(256) asaga_update_kernel(UpdateParams p) {
+  extern __shared__ double q_stash[];
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if (w >= p.workers) return;
+  double* qs = q_stash + (size_t)(threadIdx.x / G) * (size_t)p.overflow;
+
+  const uint64_t tend = p.t0 + p.T;
+  uint64_t t = p.t0 + (uint64_t)w;
+  if (t >= tend) return;
+  const uint64_t W = (uint64_t)p.workers;
+  int64_t i = sample_row(p.seed, t, p.n);
+  int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
+
+  while (true) {
+    // ---- pass 1: row entries, gathers of (x, abar, D), dot product
+    int cc[NR];
+    double aa[NR], qq[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int64_t k = lo + j * G + g;
+      if (k < hi) {
+        cc[j] = ld_nc_i32(p.cols + k);
+        aa[j] = ld_nc_f64(p.vals + k);
+      }
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int64_t k = lo + j * G + g;
+      if (k < hi) {
+        double x, ab, D;
+        ld_coord(p.st + cc[j], x, ab, D);
+        dot = fma(aa[j], x, dot);
+        qq[j] = D * fma(p.lambda_, x, ab);
+      }
+    }
+    for (int64_t k = lo + NR * G + g; k < hi; k += G) {  // long rows only
+      const int c = ld_nc_i32(p.cols + k);
+      const double a = ld_nc_f64(p.vals + k);
+      double x, ab, D;
+      ld_coord(p.st + c, x, ab, D);
+      dot = fma(a, x, dot);
+      qs[k - lo - NR * G] = D * fma(p.lambda_, x, ab);
+    }
+    const double ai = ld_cg(p.alpha + i);
+    // ---- prefetch the next sample's row bounds (read-only data)
+    const uint64_t tn = t + W;
+    int64_t in_ = 0, lon = 0, hin = 0;
+    if (tn < tend) {
+      in_ = sample_row(p.seed, tn, p.n);
+      lon = __ldg(&p.rowptr[in_]);
+      hin = __ldg(&p.rowptr[in_ + 1]);
+    }
+    // ---- scalar derivative (folded logistic) and memory difference
+    dot = group_sum<G>(dot, gmask);
+    const double sig = -1.0 / (1.0 + exp(dot));
+    const double da = sig - ai;
+    const double ngam = -p.gamma;
+    // ---- pass 2: unlocked scatter
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      const int64_t k = lo + j * G + g;
+      if (k < hi) {
+        const double u = fma(da, aa[j], qq[j]);
+        Coord* s = p.st + cc[j];
+        if (ATOMIC) {
+          red_add(&s->x, ngam * u);
+          red_add(&s->abar, da * aa[j] * p.inv_n);
+        } else {
+          st_cg(&s->x, ld_cg(&s->x) + ngam * u);
+          st_cg(&s->abar, ld_cg(&s->abar) + da * aa[j] * p.inv_n);
+        }
+      }
+    }
+    for (int64_t k = lo + NR * G + g; k < hi; k += G) {
+      const int c = ld_nc_i32(p.cols + k);
+      const double a = ld_nc_f64(p.vals + k);
+      const double u = fma(da, a, qs[k - lo - NR * G]);
+      Coord* s = p.st + c;
+      if (ATOMIC) {
+        red_add(&s->x, ngam * u);
+        red_add(&s->abar, da * a * p.inv_n);
+      } else {
+        st_cg(&s->x, ld_cg(&s->x) + ngam * u);
+        st_cg(&s->abar, ld_cg(&s->abar) + da * a * p.inv_n);
+      }
+    }
+    if (g == 0) {
+      if (ATOMIC) red_add(p.alpha + i, da);
+      else st_cg(p.alpha + i, ai + da);
+      if (p.visits) atomicAdd(p.visits + i, 1);
+    }
+    if (DET) {
+      __threadfence();
+      __syncwarp(gmask);
+    }
+    if (tn >= tend) break;
+    t = tn;
+    i = in_;
+    lo = lon;
+    hi = hin;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// A9: objective / gradient (Section 4.1).  Deterministic: fixed grid, fixed
+// per-group row order, fixed-order block partials.
+__global__ void extract_x_kernel(const Coord* __restrict__ st, double* __restrict__ x,
+                                 int64_t d) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x)
+    x[v] = st[v].x;
+}
+
+// Per row: m_i = a~_i . x, loss_i = softplus(-m_i) = log(1+exp(-b_i a_i.x)),
+// sigma~_i = -1/(1+exp(m_i)) (so sigma_i a_i = sigma~_i a~_i).
+template <int G>
+__global__ void __launch_bounds__(256)
+margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+              const double* __restrict__ vals, const double* __restrict__ x, int64_t n,
+              double* __restrict__ sig, double* __restrict__ block_loss) {
+  __shared__ double grp_loss[256 / G];
+  const int lane = threadIdx.x & 31, g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
+  const int gib = threadIdx.x / G;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / G) + gib; i < n; i += groups) {
+    const int64_t lo = rowptr[i], hi = rowptr[i + 1];
+    double m = 0.0;
+    for (int64_t k = lo + g; k < hi; k += G) m = fma(vals[k], __ldg(x + cols[k]), m);
+    m = group_sum<G>(m, gmask);
+    // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
+    const double loss = fmax(-m, 0.0) + log1p(exp(-fabs(m)));
+    acc += loss;
+    if (sig != nullptr && g == 0) sig[i] = -1.0 / (1.0 + exp(m));
+  }
+  if (g == 0) grp_loss[gib] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int j = 0; j < 256 / G; ++j) s += grp_loss[j];
+    block_loss[blockIdx.x] = s;
+  }
+}
+
+// Single block: f = (sum block_loss) / n + lambda/2 ||x||^2; also raw loss sum.
+__global__ void __launch_bounds__(1024)
+finish_objective_kernel(const double* __restrict__ block_loss, int nblocks,
+                        const double* __restrict__ x, int64_t d, int64_t n, double lambda_,
+                        double* __restrict__ f_out, double* __restrict__ loss_sum_out) {
+  __shared__ double s_loss[1024], s_sq[1024];
+  double a = 0.0, b = 0.0;
+  for (int j = threadIdx.x; j < nblocks; j += blockDim.x) a += block_loss[j];
+  for (int64_t v = threadIdx.x; v < d; v += blockDim.x) b = fma(x[v], x[v], b);
+  s_loss[threadIdx.x] = a;
+  s_sq[threadIdx.x] = b;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      s_loss[threadIdx.x] += s_loss[threadIdx.x + off];
+      s_sq[threadIdx.x] += s_sq[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (f_out) *f_out = s_loss[0] / (double)n + 0.5 * lambda_ * s_sq[0];
+    if (loss_sum_out) *loss_sum_out = s_loss[0];
+  }
+}
+
+// CSC segments: segment s covers csc entries [seg_lo[s], seg_hi[s]) of one column.
+__global__ void __launch_bounds__(256)
+colseg_kernel(const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ seg_hi,
+              int64_t nseg, const int32_t* __restrict__ csc_rows,
+              const double* __restrict__ csc_vals, const double* __restrict__ sig,
+              double* __restrict__ seg_sum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nseg;
+       s += warps) {
+    const int64_t lo = seg_lo[s], hi = seg_hi[s];
+    double acc = 0.0;
+    for (int64_t k = lo + lane; k < hi; k += 32) acc = fma(__ldg(sig + csc_rows[k]), csc_vals[k], acc);
+    acc = group_sum<32>(acc, 0xffffffffu);
+    if (lane == 0) seg_sum[s] = acc;
+  }
+}
+
+// g_v = scale * (sum of v's segments, in order) + lambda x_v.
+__global__ void colsum_kernel(const int64_t* __restrict__ seg_ptr,
+                              const double* __restrict__ seg_sum, const double* __restrict__ x,
+                              int64_t d, double inv_scale_div, double lambda_,
+                              double* __restrict__ g, int divide) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t j = seg_ptr[v]; j < seg_ptr[v + 1]; ++j) s += seg_sum[j];
+    g[v] = divide ? s / inv_scale_div + lambda_ * x[v] : s;
+  }
+}
+
+// CSC construction helpers (init-time, lazily on the first gradient call).
+__global__ void row_of_kernel(const int64_t* __restrict__ rowptr, int64_t n,
+                              int32_t* __restrict__ row_of) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += warps)
+    for (int64_t k = rowptr[i] + lane; k < rowptr[i + 1]; k += 32) row_of[k] = (int32_t)i;
+}
+
+__global__ void iota_kernel(int64_t* __restrict__ out, int64_t m) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = k;
+}
+
+__global__ void csc_gather_kernel(const int64_t* __restrict__ perm,
+                                  const int32_t* __restrict__ row_of,
+                                  const double* __restrict__ vals, int64_t m,
+                                  int32_t* __restrict__ csc_rows, double* __restrict__ csc_vals) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = perm[k];
+    csc_rows[k] = row_of[j];
+    csc_vals[k] = vals[j];
+  }
+}
+
+// seg_cnt[v] = ceil(n_v / SEG)
+__global__ void segcount_kernel(const int32_t* __restrict__ counts, int64_t d, int seg,
+                                int64_t* __restrict__ seg_cnt) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x)
+    seg_cnt[v] = ((int64_t)counts[v] + seg - 1) / seg;
+}
+
+__global__ void segfill_kernel(const int64_t* __restrict__ colptr,
+                               const int64_t* __restrict__ seg_ptr, int64_t d, int seg,
+                               int64_t* __restrict__ seg_lo, int64_t* __restrict__ seg_hi) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c0 = colptr[v], c1 = colptr[v + 1];
+    int64_t s = seg_ptr[v];
+    for (int64_t a = c0; a < c1; a += seg, ++s) {
+      seg_lo[s] = a;
+      seg_hi[s] = min(a + (int64_t)seg, c1);
+    }
+  }
+}
+
+// K5 divergence guard: flag if any x_v is not finite.
+__global__ void nonfinite_kernel(const Coord* __restrict__ st, int64_t d, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(st[v].x);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void sample_kernel(uint64_t seed, uint64_t t0, uint64_t count, uint64_t n,
+                              int64_t* __restrict__ out) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count;
+       k += (uint64_t)gridDim.x * blockDim.x)
+    out[k] = sample_row(seed, t0 + k, n);
+}
+
+// State conversions between the paper's alpha and the folded alpha~ = b alpha.
+__global__ void fold_alpha_kernel(const double* __restrict__ in, const double* __restrict__ y,
+                                  double* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = y[i] * in[i];
+}
+
+__global__ void pack_state_kernel(Coord* __restrict__ st, const double* __restrict__ x,
+                                  const double* __restrict__ ab, int64_t d) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (x) st[v].x = x[v];
+    if (ab) st[v].abar = ab[v];
+  }
+}
+
+__global__ void unpack_state_kernel(const Coord* __restrict__ st, double* __restrict__ x,
+                                    double* __restrict__ ab, double* __restrict__ D, int64_t d) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (x) x[v] = st[v].x;
+    if (ab) ab[v] = st[v].abar;
+    if (D) D[v] = st[v].D;
+  }
+}
+
+}  // namespace asaga

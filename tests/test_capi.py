@@ -1,0 +1,83 @@
+"""CPU checks of the boundary (no compute calls): libasaga.so builds for sm_100a,
+loads, and exports every symbol include/asaga.h declares; the Python binding
+covers exactly those; the product path never touches the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "asaga.h")
+PKG = os.path.join(ROOT, "paper_1606_04809_b200")
+
+
+def declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^ASAGA_API [^;]*?\b(asaga_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_1606_04809_b200 import _build
+
+    return _build.build()
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared()
+    for must in ("asaga_init", "asaga_run", "asaga_objective", "asaga_full_grad"):
+        assert must in names
+    assert len(names) >= 20
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    for name in declared():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    assert exported == set(declared())
+
+
+def test_binding_matches_header(libpath):
+    from paper_1606_04809_b200 import asaga
+
+    assert set(asaga.ABI_FUNCTIONS) == set(declared())
+    assert asaga.lib().asaga_abi_version() == 1
+    assert asaga.lib().asaga_status_string(6) == b"ASAGA_E_DIVERGED"
+    assert asaga.lib().asaga_last_error(None)  # never NULL
+
+
+def test_library_is_sm100a(libpath):
+    out = subprocess.run(["cuobjdump", "--list-elf", libpath], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_update_kernel_sass_uses_l2_atomics_and_256bit_gathers(libpath):
+    sass = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
+    assert "REDG.E.ADD.F64.RN.STRONG.GPU" in sass  # red.global.add.f64 coordinate adds
+    assert "LDG.E.ENL2.256.STRONG.GPU" in sass  # one 32-byte {x, abar, D} gather per entry
+    assert "HMMA" not in sass and "UTCHMMA" not in sass  # no tensor-core path here
+
+
+def test_product_never_imports_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_init_without_gpu_fails_loudly(libpath):
+    import numpy as np
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1606_04809_b200 import Asaga, AsagaError
+
+    with pytest.raises(AsagaError):
+        Asaga(np.array([0, 1]), np.array([0], dtype=np.int32), np.array([1.0]), np.array([1.0]),
+              1, 1.0, 1.0)

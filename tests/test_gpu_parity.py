@@ -1,0 +1,359 @@
+"""GPU parity (``-m gpu``): the CUDA path through the C-ABI against the oracle.
+
+Bars: integer/index outputs bit-exact; the deterministic
+(tau = 1) iterate within 1e-9 relative (norm-wise, per array: x, alpha, abar;
+BASELINE.json north_star); f within 1e-12 and grad f within 1e-10 relative;
+async runs checked through properties that hold for every interleaving.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+gpu = pytest.mark.gpu
+SEED = datagen.SAMPLE_SEED
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def asaga_mod():
+    import paper_1606_04809_b200 as m
+
+    return m
+
+
+def gamma_of(p):
+    return 1.0 / (3.0 * oracle.lipschitz(p, p.lam))
+
+
+SUBSETS = {
+    "c1": lambda: datagen.make("c1"),
+    "c2s": lambda: datagen.make("c2", n_rows=20_000),
+    "c3s": lambda: datagen.make("c3", n_rows=20_000),
+    "c4s": lambda: datagen.make("c4", n_rows=5_000),
+}
+
+
+@pytest.fixture(scope="module", params=list(SUBSETS))
+def prob(request):
+    return SUBSETS[request.param]()
+
+
+# ---------------------------------------------------------------------- A1 profile
+@gpu
+def test_profile_bitexact(prob):
+    m = asaga_mod()
+    a = m.Asaga.from_problem(prob, gamma_of(prob))
+    counts, D = a.profile()
+    ref_counts = oracle.column_counts(prob)
+    assert np.array_equal(counts.astype(np.int64), ref_counts)
+    assert np.array_equal(D, oracle.reweight(prob.n, ref_counts))  # IEEE division both sides
+    st = a.stats()
+    assert st["delta_r"] == ref_counts.max()
+    assert st["max_row"] == prob.row_lengths().max()
+    assert st["L"] == pytest.approx(oracle.lipschitz(prob, prob.lam), rel=1e-14)
+    a.close()
+
+
+# ---------------------------------------------------------------------- A2 sampler
+@gpu
+@pytest.mark.parametrize("n", [1, 3, 1000, 581_012, 697_641, 2_396_130])
+@pytest.mark.parametrize("seed,t0", [(SEED, 0), (2**64 - 1, 2**32 - 1000), (7, 2**45)])
+def test_sampler_bitexact(n, seed, t0):
+    import torch
+
+    m = asaga_mod()
+    count = 1_000_000
+    out = torch.empty(count, dtype=torch.int64, device="cuda")
+    m.sample_indices(seed, t0, count, n, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), oracle.sample_stream(seed, t0, count, n))
+
+
+# ---------------------------------------------------------------------- A2..A8 deterministic
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9):
+    m = asaga_mod()
+    g = gamma_of(prob)
+    a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes)
+    st = oracle.State(prob.n, prob.d)
+    D = oracle.reweight(prob.n, oracle.column_counts(prob))
+    done = 0
+    worst = 0.0
+    for c in checkpoints:
+        a.run(c - done, SEED)
+        oracle.sparse_saga(prob, prob.y, prob.lam, g, SEED, c - done, st, D)
+        done = c
+        x, alpha, ab, t = a.get_state()
+        assert t == done
+        for got, ref in ((x, st.x), (alpha, st.alpha), (ab, st.alpha_bar)):
+            e = rel(got, ref)
+            worst = max(worst, e)
+            assert e <= tol, (c, e)
+    a.close()
+    return worst
+
+
+@gpu
+def test_deterministic_c1_twenty_epochs():
+    """c1 (BASELINE config 1): 20 epochs, checked every n/10 updates."""
+    p = datagen.make("c1")
+    cps = list(range(p.n // 10, 20 * p.n + 1, p.n // 10))
+    _det_compare(p, 20 * p.n, cps)
+
+
+@gpu
+@pytest.mark.parametrize("lanes", [8, 16, 32])
+def test_deterministic_lane_groupings(lanes):
+    p = datagen.make("c1")
+    _det_compare(p, 3000, [1, 2, 37, 1000, 3000], lanes=lanes)
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c2s", "c3s", "c4s"])
+def test_deterministic_subsets(name):
+    """Config recipes at oracle size: several tiles, ragged rows, long-row overflow path."""
+    p = SUBSETS[name]()
+    _det_compare(p, 60_000, [1, 10_000, 60_000])
+
+
+@gpu
+def test_deterministic_c3_full_size_prefix():
+    """c3 at BASELINE full size: the first 1e5 updates match the oracle."""
+    p = datagen.make("c3")
+    _det_compare(p, 100_000, [50_000, 100_000])
+
+
+@gpu
+def test_run_split_equals_whole():
+    m = asaga_mod()
+    p = datagen.make("c1")
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    b = m.Asaga.from_problem(p, g, deterministic=True)
+    a.run(5000, SEED)
+    for chunk in (1, 999, 2000, 2000):
+        b.run(chunk, SEED)
+    sa, sb = a.get_state(), b.get_state()
+    for u, v in zip(sa[:3], sb[:3]):
+        assert np.array_equal(u, v)
+    assert sa[3] == sb[3] == 5000
+
+
+@gpu
+def test_device_inputs_match_host_inputs():
+    import torch
+
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=20_000)
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    t = lambda arr: torch.from_numpy(arr).cuda()
+    b = m.Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, g, deterministic=True)
+    for c in (a, b):
+        c.run(20_000, SEED)
+    for u, v in zip(a.get_state()[:3], b.get_state()[:3]):
+        assert np.array_equal(u, v)
+
+
+# ---------------------------------------------------------------------- A9 objective / gradient
+@gpu
+def test_objective_and_gradient(prob):
+    m = asaga_mod()
+    a = m.Asaga.from_problem(prob, gamma_of(prob))
+    rng = np.random.default_rng(5)
+    for x in (np.zeros(prob.d), rng.standard_normal(prob.d), 10 * rng.standard_normal(prob.d)):
+        f = a.objective(x)
+        assert f == pytest.approx(oracle.objective(prob, prob.y, prob.lam, x), rel=1e-12)
+        g = a.full_grad(x)
+        assert rel(g, oracle.full_grad(prob, prob.y, prob.lam, x)) <= 1e-10
+    # current iterate (x = NULL)
+    a.run(prob.n, SEED)
+    x = a.get_state()[0]
+    assert a.objective() == pytest.approx(oracle.objective(prob, prob.y, prob.lam, x), rel=1e-12)
+    assert rel(a.full_grad(), oracle.full_grad(prob, prob.y, prob.lam, x)) <= 1e-10
+
+
+@gpu
+def test_objective_deterministic_bits():
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=20_000)
+    a = m.Asaga.from_problem(p, gamma_of(p))
+    x = np.random.default_rng(0).standard_normal(p.d)
+    assert a.objective(x) == a.objective(x)
+    assert np.array_equal(a.full_grad(x), a.full_grad(x))
+
+
+@gpu
+def test_partial_obj_grad_shards_sum_to_whole():
+    """Row shards' partial outputs sum to the whole-problem result (multi-GPU math, 1 GPU)."""
+    import torch
+
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=20_000)
+    x = np.random.default_rng(2).standard_normal(p.d)
+    xd = torch.from_numpy(x).cuda()
+    total = torch.zeros(p.d + 1, dtype=torch.float64, device="cuda")
+    bounds = [0, 7000, 13001, p.n]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        sub = p.subset_rows(np.arange(lo, hi))
+        a = m.Asaga.from_problem(sub, 1.0, lam=p.lam)
+        out = torch.empty(p.d + 1, dtype=torch.float64, device="cuda")
+        a.partial_obj_grad(xd, out)
+        torch.cuda.synchronize()
+        total += out
+        a.close()
+    tot = total.cpu().numpy()
+    f = tot[p.d] / p.n + 0.5 * p.lam * x @ x
+    g = tot[:p.d] / p.n + p.lam * x
+    assert f == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+    assert rel(g, oracle.full_grad(p, p.y, p.lam, x)) <= 1e-10
+
+
+# ---------------------------------------------------------------------- async properties
+def _fstar(p):
+    st = oracle.sparse_saga(p, p.y, p.lam, gamma_of(p), SEED, 300 * p.n)
+    f = oracle.objective(p, p.y, p.lam, st.x)
+    gn = np.linalg.norm(oracle.full_grad(p, p.y, p.lam, st.x))
+    assert gn ** 2 / (2 * p.lam) <= 1e-10
+    return f
+
+
+def _epochs_to(p, f_star, runner, tol=1e-6, max_epochs=60):
+    """First 0.1-epoch checkpoint with f - f* <= tol (reading R12); runner(k) runs k updates."""
+    step = p.n // 10
+    for j in range(1, 10 * max_epochs + 1):
+        f = runner(step)
+        if f - f_star <= tol:
+            return j / 10
+    return float("inf")
+
+
+@gpu
+@pytest.mark.parametrize("conc", [1, 4, 16])
+def test_async_c1_epochs_within_1p5x_oracle(conc):
+    m = asaga_mod()
+    p = datagen.make("c1")
+    fs = _fstar(p)
+    g = gamma_of(p)
+    st = oracle.State(p.n, p.d)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+
+    def orun(k):
+        oracle.sparse_saga(p, p.y, p.lam, g, SEED, k, st, D)
+        return oracle.objective(p, p.y, p.lam, st.x)
+
+    e_or = _epochs_to(p, fs, orun)
+    a = m.Asaga.from_problem(p, g, concurrency=conc)
+
+    def grun(k):
+        a.run(k, SEED)
+        return a.objective()
+
+    e_gpu = _epochs_to(p, fs, grun)
+    assert e_gpu <= 1.5 * e_or, (e_gpu, e_or)
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_async_sample_stream_and_quiescent_identity(name):
+    """Every t is processed exactly once (visit histogram == oracle's stream histogram,
+    bit-exact) and, once quiescent, abar == (1/n) sum alpha_i a_i (no lost update)."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 5 * p.n + 12345
+    a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True)
+    a.run(T, SEED)
+    visits = a.sample_counts()
+    ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
+    assert np.array_equal(visits.astype(np.int64), ref)
+    x, alpha, ab, t = a.get_state()
+    assert t == T
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    ref_ab = A.T @ alpha / p.n
+    assert rel(ab, ref_ab) <= 1e-10
+    assert np.all(np.isfinite(x))
+
+
+@gpu
+def test_async_fixed_point_is_stationary():
+    """P9 on the GPU: at the optimum state every (async) update is zero."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = datagen.make("c1")
+    st = oracle.sparse_saga(p, p.y, p.lam, gamma_of(p), SEED, 400 * p.n)
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    xs = st.x
+    alpha = -p.y / (1.0 + np.exp(p.y * (A @ xs)))
+    ab = A.T @ alpha / p.n
+    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=32)
+    a.set_state(xs, alpha, ab, 0)
+    a.run(10 * p.n, SEED)
+    x = a.get_state()[0]
+    assert np.abs(x - xs).max() <= 1e-10
+
+
+@gpu
+def test_non_atomic_ablation_loses_updates():
+    """App. E: without atomic adds, concurrent updates to the hot columns
+    are lost, so abar drifts from (1/n) sum alpha_i a_i; with atomics it does not."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = datagen.make("c2", n_rows=20_000)
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    errs = {}
+    for atomic in (True, False):
+        a = m.Asaga.from_problem(p, gamma_of(p), atomic=atomic, concurrency=1024)
+        a.run(20 * p.n, SEED)
+        _, alpha, ab, _ = a.get_state()
+        errs[atomic] = rel(ab, A.T @ alpha / p.n)
+    assert errs[True] <= 1e-10
+    assert errs[False] >= 100 * max(errs[True], 1e-14)
+
+
+# ---------------------------------------------------------------------- boundary errors
+@gpu
+def test_errors():
+    m = asaga_mod()
+    E = m.AsagaError
+    ok = dict(indptr=np.array([0, 2, 3]), indices=np.array([0, 1, 1], dtype=np.int32),
+              data=np.array([1.0, 1.0, 1.0]), y=np.array([1.0, -1.0]))
+
+    def mk(**kw):
+        a = dict(ok)
+        a.update(kw)
+        return m.Asaga(a["indptr"], a["indices"], a["data"], a["y"], kw.get("d", 2),
+                       kw.get("lam", 0.5), kw.get("gamma", 1.0))
+
+    mk().close()
+    cases = [
+        (dict(indices=np.array([1, 0, 1], dtype=np.int32)), "ASAGA_E_BAD_CSR", "row 0"),
+        (dict(indices=np.array([0, 0, 1], dtype=np.int32)), "ASAGA_E_BAD_CSR", "row 0"),
+        (dict(indices=np.array([0, 1, 2], dtype=np.int32)), "ASAGA_E_BAD_CSR", "row 1"),
+        (dict(indptr=np.array([0, 3, 3])), "ASAGA_E_BAD_CSR", "row 1"),
+        (dict(y=np.array([1.0, 0.0])), "ASAGA_E_BAD_LABEL", "row 1"),
+        (dict(data=np.array([1.0, np.nan, 1.0])), "ASAGA_E_BAD_CSR", "row 0"),
+        (dict(lam=0.0), "ASAGA_E_INVALID_ARG", "lambda"),
+        (dict(gamma=-1.0), "ASAGA_E_INVALID_ARG", "gamma"),
+        (dict(indptr=np.array([0, 2, 4])), "ASAGA_E_BAD_CSR", "indptr"),
+    ]
+    for kw, name, frag in cases:
+        with pytest.raises(E) as ei:
+            mk(**kw)
+        assert ei.value.name == name, (kw, ei.value)
+        assert frag in str(ei.value), (kw, ei.value)
+    a = mk()
+    with pytest.raises(E) as ei:
+        a.sample_counts()
+    assert ei.value.name == "ASAGA_E_STATE"
+    a.set_gamma(1e6)
+    with pytest.raises(E) as ei:
+        a.run(2000, SEED)
+    assert ei.value.name == "ASAGA_E_DIVERGED"

@@ -1,0 +1,249 @@
+// microbench.cu -- roofline denominators for the ASAGA update kernel on B200
+// (SURVEY.md section 8(d), M1-M5).  Prints one JSON object.
+//   M0 hbm_copy      cudaMemcpy D2D (r+w bytes), sanity vs MEASURED_PEAKS.json
+//   M1 hbm_rows      random rows of s entries (int32 index + fp64 value) from a
+//                    4+ GB CSR-like array: the A3 row fetch
+//   M2 l2_gather     random 256-bit .cg loads of 32-byte {x, abar, D} records,
+//                    L2-resident tables of d records: the A4/A6 gathers
+//   M3 red_distinct  red.global.add.f64 to uniformly random records (d records)
+//   M4 red_same      red.global.add.f64 to k in {1, 10} addresses (hot columns)
+//   M5 red_zipf      red.global.add.f64 with Zipf(s) column popularity over d
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/microbench tools/microbench.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cmath>
+#include <random>
+#include <string>
+#include <vector>
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e = (x);                                                            \
+    if (e != cudaSuccess) {                                                         \
+      fprintf(stderr, "%s: %s (line %d)\n", #x, cudaGetErrorString(e), __LINE__);   \
+      exit(1);                                                                      \
+    }                                                                               \
+  } while (0)
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return x;
+}
+
+struct __align__(32) Rec { double a, b, c, d; };
+
+__global__ void k_rows(const int32_t* __restrict__ idx, const double* __restrict__ val, uint64_t N,
+                       int s, int rows_per_warp, uint32_t salt, double* out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  double acc = 0;
+  for (int r = 0; r < rows_per_warp; ++r) {
+    uint64_t start = ((uint64_t)hash32((uint32_t)(w * rows_per_warp + r) ^ salt) * 2654435761ull) % (N - s);
+    for (int k = lane; k < s; k += 32) acc += __ldg(idx + start + k) * __ldg(val + start + k);
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+__global__ void k_gather(const Rec* __restrict__ tab, uint32_t d, int iters, uint32_t salt, double* out) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc = 0;
+#pragma unroll 4
+  for (int it = 0; it < iters; ++it) {
+    uint32_t v = hash32(tid * 977u + it * 0x9E3779B9u + salt) % d;
+    double a, b, c, e;
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(e) : "l"(tab + v));
+    acc += a + b + c;
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
+__global__ void k_red_random(double* tab, uint32_t d, uint32_t stride, int iters, uint32_t salt) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+#pragma unroll 4
+  for (int it = 0; it < iters; ++it) {
+    uint32_t v = hash32(tid * 977u + it * 0x9E3779B9u + salt) % d;
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)v * stride), "d"(1.0) : "memory");
+  }
+}
+
+__global__ void k_red_same(double* tab, uint32_t k, uint32_t stride, int iters) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+    uint32_t v = (tid + it) % k;
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)v * stride), "d"(1.0) : "memory");
+  }
+}
+
+__global__ void k_red_list(double* tab, const uint32_t* __restrict__ list, uint64_t m, uint32_t stride) {
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x)
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)__ldg(list + j) * stride), "d"(1.0) : "memory");
+}
+
+template <typename F>
+float best_ms(F f, int reps = 5) {
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  f();  // warm-up
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(a));
+    f();
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    best = std::min(best, ms);
+  }
+  CK(cudaGetLastError());
+  return best;
+}
+
+int main(int argc, char** argv) {
+  int dev = 0;
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  const int sms = prop.multiProcessorCount;
+  int clk = 0, memclk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  cudaDeviceGetAttribute(&memclk, cudaDevAttrMemoryClockRate, dev);
+  std::string js = "{";
+  char buf[512];
+  snprintf(buf, sizeof buf,
+           "\"device\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"persisting_l2_max\": %d, "
+           "\"smem_per_sm\": %zu, \"sm_clock_khz\": %d, \"mem_clock_khz\": %d",
+           prop.name, sms, prop.l2CacheSize, prop.persistingL2CacheMaxSize,
+           prop.sharedMemPerMultiprocessor, clk, memclk);
+  js += buf;
+
+  // M0 copy
+  {
+    size_t bytes = (size_t)2 << 30;
+    void *a, *b;
+    CK(cudaMalloc(&a, bytes));
+    CK(cudaMalloc(&b, bytes));
+    CK(cudaMemset(a, 1, bytes));
+    float ms = best_ms([&] { CK(cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice)); });
+    snprintf(buf, sizeof buf, ", \"hbm_copy_gbs\": %.1f", 2.0 * bytes / ms / 1e6);
+    js += buf;
+    CK(cudaFree(a));
+    CK(cudaFree(b));
+  }
+  double* out;
+  CK(cudaMalloc(&out, 64));
+  // M1 random rows
+  {
+    const uint64_t N = (uint64_t)1 << 28;  // 268M entries: 1 GiB idx + 2 GiB val
+    int32_t* idx;
+    double* val;
+    CK(cudaMalloc(&idx, N * 4));
+    CK(cudaMalloc(&val, N * 8));
+    CK(cudaMemset(idx, 0, N * 4));
+    CK(cudaMemset(val, 0, N * 8));
+    js += ", \"hbm_rows\": {";
+    int first = 1;
+    for (int s : {12, 73, 116}) {
+      const int rpw = 64;
+      const int blocks = sms * 8, threads = 256;
+      const double rows = (double)blocks * threads / 32 * rpw;
+      float ms = best_ms([&] { k_rows<<<blocks, threads>>>(idx, val, N, s, rpw, 17u, out); });
+      snprintf(buf, sizeof buf, "%s\"s%d\": {\"rows_per_s\": %.4g, \"useful_gbs\": %.1f}", first ? "" : ", ", s,
+               rows / ms * 1e3, rows * s * 12.0 / ms / 1e6);
+      js += buf;
+      first = 0;
+    }
+    js += "}";
+    CK(cudaFree(idx));
+    CK(cudaFree(val));
+  }
+  // M2 gathers, M3 random REDs
+  {
+    js += ", \"l2_gather\": {";
+    int first = 1;
+    for (uint32_t d : {54u, 47236u, 3231961u}) {
+      Rec* tab;
+      CK(cudaMalloc(&tab, (size_t)d * sizeof(Rec)));
+      CK(cudaMemset(tab, 0, (size_t)d * sizeof(Rec)));
+      const int blocks = sms * 8, threads = 256, iters = 256;
+      const double g = (double)blocks * threads * iters;
+      float ms = best_ms([&] { k_gather<<<blocks, threads>>>(tab, d, iters, 3u, out); });
+      snprintf(buf, sizeof buf, "%s\"d%u\": {\"gathers_per_s\": %.4g, \"sector_gbs\": %.1f}", first ? "" : ", ", d,
+               g / ms * 1e3, g * 32.0 / ms / 1e6);
+      js += buf;
+      first = 0;
+      CK(cudaFree(tab));
+    }
+    js += "}, \"red_distinct\": {";
+    first = 1;
+    for (uint32_t d : {47236u, 3231961u}) {
+      double* tab;
+      CK(cudaMalloc(&tab, (size_t)d * 32));
+      CK(cudaMemset(tab, 0, (size_t)d * 32));
+      const int blocks = sms * 8, threads = 256, iters = 256;
+      const double g = (double)blocks * threads * iters;
+      float ms = best_ms([&] { k_red_random<<<blocks, threads>>>(tab, d, 4, iters, 5u); });
+      snprintf(buf, sizeof buf, "%s\"d%u\": {\"reds_per_s\": %.4g}", first ? "" : ", ", d, g / ms * 1e3);
+      js += buf;
+      first = 0;
+      CK(cudaFree(tab));
+    }
+    js += "}, \"red_same\": {";
+    first = 1;
+    for (uint32_t k : {1u, 10u, 54u}) {
+      double* tab;
+      CK(cudaMalloc(&tab, (size_t)k * 32));
+      CK(cudaMemset(tab, 0, (size_t)k * 32));
+      const int blocks = sms * 4, threads = 256, iters = 64;
+      const double g = (double)blocks * threads * iters;
+      float ms = best_ms([&] { k_red_same<<<blocks, threads>>>(tab, k, 4, iters); });
+      snprintf(buf, sizeof buf, "%s\"k%u\": {\"reds_per_s\": %.4g, \"per_address\": %.4g}", first ? "" : ", ", k,
+               g / ms * 1e3, g / ms * 1e3 / k);
+      js += buf;
+      first = 0;
+      CK(cudaFree(tab));
+    }
+    js += "}";
+  }
+  // M5 Zipf RED pattern
+  {
+    js += ", \"red_zipf\": {";
+    int first = 1;
+    struct Z { uint32_t d; double s; const char* name; };
+    for (Z z : {Z{47236u, 1.1, "c3"}, Z{3231961u, 1.0, "c4"}}) {
+      std::vector<double> cdf(z.d);
+      double acc = 0;
+      for (uint32_t k = 0; k < z.d; ++k) { acc += std::pow((double)(k + 1), -z.s); cdf[k] = acc; }
+      for (auto& c : cdf) c /= acc;
+      std::mt19937_64 rng(160604809);
+      std::uniform_real_distribution<double> U(0.0, 1.0);
+      std::vector<uint32_t> perm(z.d);
+      for (uint32_t k = 0; k < z.d; ++k) perm[k] = k;
+      std::shuffle(perm.begin(), perm.end(), rng);
+      const uint64_t m = (uint64_t)1 << 26;
+      std::vector<uint32_t> list(m);
+      for (uint64_t j = 0; j < m; ++j)
+        list[j] = perm[std::min<uint32_t>((uint32_t)(std::upper_bound(cdf.begin(), cdf.end(), U(rng)) - cdf.begin()), z.d - 1)];
+      uint32_t* dl;
+      double* tab;
+      CK(cudaMalloc(&dl, m * 4));
+      CK(cudaMemcpy(dl, list.data(), m * 4, cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&tab, (size_t)z.d * 32));
+      CK(cudaMemset(tab, 0, (size_t)z.d * 32));
+      float ms = best_ms([&] { k_red_list<<<sms * 16, 256>>>(tab, dl, m, 4); });
+      snprintf(buf, sizeof buf, "%s\"%s\": {\"reds_per_s\": %.4g}", first ? "" : ", ", z.name, (double)m / ms * 1e3);
+      js += buf;
+      first = 0;
+      CK(cudaFree(dl));
+      CK(cudaFree(tab));
+    }
+    js += "}";
+  }
+  js += "}";
+  printf("%s\n", js.c_str());
+  return 0;
+}
