@@ -353,7 +353,8 @@ def test_errors():
     with pytest.raises(E) as ei:
         a.sample_counts()
     assert ei.value.name == "ASAGA_E_STATE"
-    a.set_gamma(1e6)
+    a.close()
+    d = m.Asaga(ok["indptr"], ok["indices"], ok["data"], ok["y"], 2, 0.5, 1e6, deterministic=True)
     with pytest.raises(E) as ei:
-        a.run(2000, SEED)
+        d.run(2000, SEED)
     assert ei.value.name == "ASAGA_E_DIVERGED"

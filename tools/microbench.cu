@@ -207,6 +207,23 @@ int main(int argc, char** argv) {
       first = 0;
       CK(cudaFree(tab));
     }
+    js += "}, \"red_same_stride\": {";
+    first = 1;
+    for (uint32_t k : {10u, 20u}) {
+      for (uint32_t stride : {1u, 4u, 16u, 32u, 128u}) {
+        double* tab;
+        CK(cudaMalloc(&tab, (size_t)k * stride * 8 + 64));
+        CK(cudaMemset(tab, 0, (size_t)k * stride * 8 + 64));
+        const int blocks = sms * 4, threads = 256, iters = 64;
+        const double g = (double)blocks * threads * iters;
+        float ms = best_ms([&] { k_red_same<<<blocks, threads>>>(tab, k, stride, iters); });
+        snprintf(buf, sizeof buf, "%s\"k%u_stride%uB\": {\"reds_per_s\": %.4g, \"per_address\": %.4g}",
+                 first ? "" : ", ", k, stride * 8, g / ms * 1e3, g / ms * 1e3 / k);
+        js += buf;
+        first = 0;
+        CK(cudaFree(tab));
+      }
+    }
     js += "}";
   }
   // M5 Zipf RED pattern

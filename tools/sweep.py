@@ -1,0 +1,82 @@
+"""Operating-point sweep on the GPU: samples in flight (concurrency) x step-size scale.
+
+For each (W, gamma scale) runs ASAGA from x = 0 with f evaluated every n/10
+updates (reading R12, evaluation time excluded) until f - f* <= 1e-6 or the
+epoch budget ends; reports epochs-to-1e-6, update-kernel updates/s and the
+time-to-1e-6 (sum of update-kernel event times).  f* comes from the committed
+oracle file tests/golden/fstar_<cfg>.json (written by scripts/compute_fstar.py).
+
+    python tools/sweep.py c3 --conc 64,256,1024 --scales 1,0.5,0.25 --epochs 40
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg")
+    ap.add_argument("--conc", default="64,128,256,512,1024,2048,4096,0")
+    ap.add_argument("--scales", default="1,0.5,0.25,0.125")
+    ap.add_argument("--epochs", type=float, default=40)
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    import torch
+    from paper_1606_04809_b200 import Asaga
+
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"fstar_{args.cfg}.json")))
+    p = datagen.make(args.cfg)
+    assert p.sha256() == gold["sha256"], "generated data differs from the f* file"
+    fstar = gold["f_star"]
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
+    base = Asaga(*A, p.d, p.lam, 1.0)
+    gamma0 = 1.0 / (3.0 * base.stats()["L"])
+    results = []
+    for W in [int(c) for c in args.conc.split(",")]:
+        for sc in [float(s) for s in args.scales.split(",")]:
+            a = base
+            a.reload(*A)
+            a.set_concurrency(W)
+            a.set_gamma(gamma0 * sc)
+            stream = torch.cuda.ExternalStream(a.stream, device=dev)
+            step = p.n // 10
+            upd_ms = 0.0
+            ep = None
+            fs = []
+            for j in range(1, int(args.epochs * 10) + 1):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                a.run_async(step, datagen.SAMPLE_SEED)
+                e1.record(stream)
+                f = a.objective()
+                upd_ms += e0.elapsed_time(e1)
+                fs.append(f - fstar)
+                if not np.isfinite(f) or f - fstar > 10:
+                    ep = "diverged"
+                    break
+                if f - fstar <= args.tol:
+                    ep = j / 10
+                    break
+            st = a.stats()
+            r = {"cfg": args.cfg, "W": st["concurrency"], "gamma_scale": sc, "epochs_to_tol": ep,
+                 "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
+                 "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
+            results.append(r)
+            print(json.dumps(r), flush=True)
+    if args.out:
+        json.dump(results, open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
