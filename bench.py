@@ -1,18 +1,22 @@
-"""bench.py -- ASAGA hot path on B200: updates/s of one full step of the path.
+"""bench.py -- the ASAGA hot path on B200, through the C-ABI (libasaga.so).
 
 A "step" = one pass of every SURVEY.md section 8(a) row over one batch of
-synthetic input, all through the C-ABI (libasaga.so):
-    A0+A1  asaga_reload_device  (validate, fold labels, n_v / D / L)     2 kernels
-    A2-A8  asaga_run_async(n)   (one epoch = n ASAGA updates)           1 kernel
-    A9     asaga_objective_device (f at the new iterate)                3 kernels
-value = n updates / step time (device time, CUDA events on the context's
-stream, max over ranks).  L2 is flushed (a 512 MiB write) between steps,
-outside the timed events.  N > 1 ranks run independent lambda-sweep
-instances (lambda_r = 10^-r / n): weak scaling, no collective on
-the data path.
+synthetic input:
+    A0+A1  asaga_reload_device     validate, fold labels, n_v / D / L     3 kernels
+    A2-A8  asaga_run_async(n)      one epoch = n ASAGA updates            1 kernel
+    A9     asaga_objective_device  f at the new iterate                   2 kernels
+value = n updates / step time (CUDA events on the context's stream, summed
+over the K timed steps, max over ranks).  512 MiB of L2 is overwritten
+between steps, outside the timed events.  The update kernel runs at the
+workload's convergent operating point (samples in flight W, step gamma =
+scale / (3L)) chosen from the sweeps in profiles/ (DESIGN.md "Operating
+point"); the line also reports time-to-1e-6 from x = 0 at that point.
+
+N > 1 ranks run independent lambda-sweep instances (lambda_r = 10^-r / n,
+SURVEY 8(e)): weak scaling, no collective on the data path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
-                    [--concurrency 0] [--impl ours|reference]
+                    [--concurrency W] [--gamma-scale s] [--impl ours|reference]
 """
 from __future__ import annotations
 
@@ -31,11 +35,16 @@ sys.path.insert(0, ROOT)
 
 import datagen  # noqa: E402
 
-# Algorithmic bytes per update, labels folded:
-#   HBM   : row (4 B index + 8 B value) * s + indptr pair 16 B + alpha_i RMW 16 B
-#   L2    : one 32-byte {x, abar, D} sector gather per entry + 2 REDs per entry
+# Convergent operating points (W samples in flight, gamma scale vs 1/(3L)) from
+# tools/sweep.py on B200 (profiles/r01_operating_point.md): the fastest
+# time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
+OPERATING_POINT = {"c1": (16, 1.0), "c2": (1024, 0.125), "c3": (256, 0.35), "c4": (256, 0.25)}
+
+
 def hbm_bytes_per_update(mean_s: float) -> float:
-    return 12.0 * mean_s + 16.0 + 16.0
+    """Algorithmic HBM bytes of one update: the row
+    (int32 index + fp64 value + fp64 D) * s, the indptr pair, the alpha_i RMW."""
+    return 20.0 * mean_s + 16.0 + 16.0
 
 
 def parse():
@@ -44,18 +53,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
-    ap.add_argument("--concurrency", type=int, default=0, help="samples in flight (0 = auto)")
+    ap.add_argument("--concurrency", type=int, default=None, help="samples in flight")
+    ap.add_argument("--gamma-scale", type=float, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-6 run")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
-
-
-def dist_setup(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
 
 
 class ClockSampler:
@@ -94,8 +98,9 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        fl = lambda v: float(v) if v.replace(".", "", 1).isdigit() else None
+        sm = [fl(r[0]) for r in self.rows if fl(r[0]) is not None]
+        mx = [fl(r[1]) for r in self.rows if fl(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[j] for r in self.rows for j in range(4)
                           if len(r) > 3 + j and r[3 + j].lower() == "active"})
@@ -104,20 +109,18 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def peaks():
+def load_json(*parts):
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
-    except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
-
-
-def ncu_traffic(workload: str):
-    """dram bytes per launch of the update kernel from the committed ncu capture, if any."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return t.get(workload)
+        return json.load(open(os.path.join(ROOT, *parts)))
     except Exception:
         return None
+
+
+def peaks():
+    pk = load_json("MEASURED_PEAKS.json")
+    if pk:
+        return pk, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
 def cpu_baseline(p, gamma, seconds: float):
@@ -136,10 +139,11 @@ def cpu_baseline(p, gamma, seconds: float):
     dt = time.perf_counter() - t0
     return {"value": T / dt, "unit": "updates/s", "cores": 1, "kind": "oracle",
             "sample": f"{T} sequential updates (t={probe}..{probe + T - 1}) of {p.name} from x=0 "
-                      f"after a {probe}-update probe; {dt:.1f} s on 1 host thread ({os.cpu_count()} cores on host)"}
+                      f"after a {probe}-update probe, gamma=1/(3L); {dt:.1f} s on 1 host thread "
+                      f"of {os.cpu_count()}"}
 
 
-def run_reference(args, world, rank):
+def run_reference(args, rank):
     """--impl reference: the oracle as it stands, on the host cores, rank 0 only."""
     if rank != 0:
         return
@@ -149,7 +153,7 @@ def run_reference(args, world, rank):
     gamma = 1.0 / (3.0 * oracle.lipschitz(p, p.lam))
     st = oracle.State(p.n, p.d)
     D = oracle.reweight(p.n, oracle.column_counts(p))
-    per_step = max(1000, min(p.n, 2_000_000 // max(args.steps + args.warmup, 1)))
+    per_step = max(1000, min(p.n, 3_000_000 // max(args.steps + args.warmup, 1)))
     for _ in range(args.warmup):
         oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
     t0 = time.perf_counter()
@@ -157,7 +161,8 @@ def run_reference(args, world, rank):
         oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
     dt = time.perf_counter() - t0
     v = per_step * args.steps / dt
-    sample = f"{args.steps} steps x {per_step} sequential updates of {p.name} (bounded sample of an epoch of n={p.n})"
+    sample = (f"{args.steps} steps x {per_step} sequential updates of {p.name} "
+              f"(a bounded sample of the n={p.n}-update epoch), 1 host thread of {os.cpu_count()}")
     print(json.dumps({
         "impl": "reference", "metric": "ASAGA updates/s", "value": v, "unit": "updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -170,11 +175,41 @@ def run_reference(args, world, rank):
     }))
 
 
+def time_to_target(a, p, stream, seed, tol=1e-6, max_epochs=40.0):
+    """From x = 0: epochs and update-kernel seconds until f - f* <= tol, f checked every
+    n/10 updates (reading R12; evaluation excluded). f* from the oracle's golden file."""
+    import torch
+
+    gold = load_json("tests", "golden", f"fstar_{p.name}.json")
+    if gold is None or gold.get("sha256") != p.sha256():
+        return None
+    fstar = gold["f_star"]
+    step = p.n // 10
+    ms = 0.0
+    a.set_state(np.zeros(p.d), np.zeros(p.n), np.zeros(p.d), 0)
+    for j in range(1, int(max_epochs * 10) + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        a.run_async(step, seed)
+        e1.record(stream)
+        f = a.objective()
+        ms += e0.elapsed_time(e1)
+        if f - fstar <= tol:
+            return {"epochs": j / 10, "seconds": ms / 1e3, "tol": tol, "f_star": fstar,
+                    "oracle_epochs": gold["oracle_epochs_to_1e-6"],
+                    "within_1p5x_oracle_epochs": j / 10 <= 1.5 * gold["oracle_epochs_to_1e-6"]}
+        if not np.isfinite(f):
+            break
+    return {"epochs": None, "seconds": None, "tol": tol, "f_star": fstar, "last_subopt": f - fstar}
+
+
 def main():
     args = parse()
-    world, rank, local = dist_setup(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, world, rank)
+        run_reference(args, rank)
         return
     import torch
     import torch.distributed as dist
@@ -185,13 +220,16 @@ def main():
     from paper_1606_04809_b200 import Asaga
 
     p = datagen.make(args.workload)
+    W0, gs0 = OPERATING_POINT[args.workload]
+    W = args.concurrency if args.concurrency is not None else W0
+    gscale = args.gamma_scale if args.gamma_scale is not None else gs0
     lam = p.lam * (10.0 ** (-rank))  # rank 0: lambda = 1/n (the BASELINE config)
-    # L = max ||a_i||^2/4 + lambda; rows are unit-norm (reading R7) -> gamma = 1/(3L)
     dev = torch.device("cuda", local)
-    t = lambda a: torch.from_numpy(a).to(dev)
+    t = lambda arr: torch.from_numpy(arr).to(dev)
     indptr, indices, data, y = t(p.indptr), t(p.indices), t(p.data), t(p.y)
-    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=args.concurrency, device=local)
-    gamma = 1.0 / (3.0 * a.stats()["L"])
+    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local)
+    L = a.stats()["L"]
+    gamma = gscale / (3.0 * L)
     a.set_gamma(gamma)
     stream = torch.cuda.ExternalStream(a.stream, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -230,19 +268,19 @@ def main():
     upd_ms = [e[1].elapsed_time(e[2]) for e in all_evs]
     ing_ms = [e[0].elapsed_time(e[1]) for e in all_evs]
     obj_ms = [e[2].elapsed_time(e[3]) for e in all_evs]
-    total_ms = float(sum(step_ms))
     f_final = float(f_dev.item())
-    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    tmax = torch.tensor([float(sum(step_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     total_ms_max = float(tmax.item())
     value = world * p.n * args.steps / (total_ms_max / 1e3)
 
-    # ---- e2e: the same step through the host-buffer C-ABI path (pinned host inputs,
-    # H2D copies and the D2H read of f inside the timed region)
+    # ---- e2e: the same step through the host-buffer C-ABI path (pinned host inputs;
+    # the H2D copies and the D2H read of f inside the timed region)
     hp = [torch.from_numpy(arr).pin_memory() for arr in (p.indptr, p.indices, p.data, p.y)]
     h2d = sum(x.numel() * x.element_size() for x in hp)
     e2e_ms = []
+    f_host = None
     for k in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -258,38 +296,56 @@ def main():
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = world * p.n * args.steps / (float(e2e_t.item()) / 1e3)
 
+    ttt = None
+    if rank == 0 and not args.no_ttt:
+        a.reload(indptr, indices, data, y)
+        ttt = time_to_target(a, p, stream, seed)
+
     if rank == 0:
         st = a.stats()
         pk, pk_kind = peaks()
         mean_s = p.nnz / p.n
-        bytes_launch = hbm_bytes_per_update(mean_s) * p.n
+        bpu = hbm_bytes_per_update(mean_s)
         upd_avg_s = float(np.mean(upd_ms)) / 1e3
-        achieved = bytes_launch / upd_avg_s / 1e9
+        ups = p.n / upd_avg_s
+        achieved = bpu * p.n / upd_avg_s / 1e9
+        mb = load_json("profiles", "microbench_b200.json") or {}
+        hot = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair")
         out = {
-            "metric": "ASAGA updates/s (one step = ingest + 1 epoch of updates + objective)",
+            "metric": "ASAGA updates/s (one step = ingest A0-A1 + one epoch of updates A2-A8 + objective A9)",
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
+            "data": "synthetic (datagen recipe, DESIGN.md 'Input recipe')",
             "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz,
                        "samples_in_flight": st["concurrency"], "lanes_per_sample": st["lanes_per_sample"],
-                       "gamma": gamma, "lambda": "10^-rank / n", "l2_flush": "512 MiB write between steps",
+                       "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale, "lambda": "10^-rank / n",
+                       "l2_flush": "512 MiB write between steps (outside the timed events)",
                        "parallelism": f"{world} independent lambda-sweep instances" if world > 1 else "1 GPU"},
             "breakdown_ms": {"ingest_A0_A1": float(np.mean(ing_ms)), "updates_A2_A8": float(np.mean(upd_ms)),
                              "objective_A9": float(np.mean(obj_ms))},
-            "update_kernel_updates_per_s": p.n / upd_avg_s,
+            "update_kernel_updates_per_s": ups,
+            "time_to_1e-6": ttt,
             "f_after_step": f_final,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(p.name),
-                         "kernel": "asaga_update_kernel",
-                         "bytes_per_update": hbm_bytes_per_update(mean_s), "peak_source": pk_kind},
+                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "kernel": "asaga_update_kernel", "bytes_per_update": bpu,
+                         "peak_source": pk_kind},
+            "roofline_hot_line": {
+                "bound": "L2 atomic service of the hottest feature's line (1 pair load + 2 REDs per update)",
+                "achieved": ups, "peak": hot, "unit": "updates/s",
+                "frac": (ups / hot) if hot else None,
+                "peak_source": "tools/microbench hot_pair.k10 (profiles/microbench_b200.json)"},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "f_host": f_host},
             "gpu_launches": 6 * args.steps,
             "clocks": clk.summary(),
         }
+        tr = load_json("profiles", "traffic.json") or {}
+        if p.name in tr:
+            out["roofline"]["traffic"] = tr[p.name]
         if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(p, gamma, args.cpu_seconds)
+            out["cpu_baseline"] = cpu_baseline(p, 1.0 / (3.0 * L), args.cpu_seconds)
         print(json.dumps(out))
     a.close()
     if world > 1:

@@ -29,12 +29,19 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
+TIMING_LIB = os.path.join(HERE, "libasaga_timing.so")
+
+
+def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
+    """Build libasaga.so; timing=True builds the clock64-instrumented profiling variant
+    libasaga_timing.so (tools/, never loaded by the product path)."""
+    lib = TIMING_LIB if timing else LIB
+    if not force and os.path.exists(lib) and all(os.path.getmtime(p) <= os.path.getmtime(lib) for p in DEPS):
+        return lib
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
+    tmp = lib + f".tmp{os.getpid()}"
+    extra = ["-DASAGA_TIMING"] if timing else []
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp, *SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
@@ -44,8 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (exit {res.returncode}); see {log}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -92,11 +92,13 @@ ABI_FUNCTIONS = {
 
 
 def _load():
-    if not os.path.exists(LIB):
+    # ASAGA_LIB selects a profiling build (tools/phase_timing.py); default: the in-tree build
+    path = os.environ.get("ASAGA_LIB", LIB)
+    if not os.path.exists(path):
         raise ImportError(
-            f"libasaga.so not found at {LIB}: build it with `python -c 'import __graft_entry__ as g; "
+            f"libasaga.so not found at {path}: build it with `python -c 'import __graft_entry__ as g; "
             "g.build()'` (there is no CPU fallback)")
-    lib = ctypes.CDLL(LIB)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in ABI_FUNCTIONS.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -50,12 +51,14 @@ struct asaga_ctx {
   int32_t* cols = nullptr;
   double* vals = nullptr;  // folded a~ = b a
   double* y = nullptr;
-  Coord* st = nullptr;
+  double2* xa = nullptr;   // {x_v, abar_v} pairs at xa[v * S]
+  int S = 1;               // pair stride
+  double* D = nullptr;     // reweighting n / n_v
+  double* dv = nullptr;    // D_{c_k} per stored entry
   double* alpha = nullptr;  // folded alpha~ = b alpha
   int32_t* counts = nullptr;
   int32_t* visits = nullptr;
   // scratch
-  double* xdense = nullptr;
   double* sig = nullptr;
   double* block_loss = nullptr;
   double* scal = nullptr;  // [0] f, [1] loss sum
@@ -77,7 +80,8 @@ struct asaga_ctx {
   // update-kernel launch shape
   int lanes = 32, nr = 1;
   int overflow = 0;
-  size_t smem = 0;
+  size_t smem = 0;         // dynamic shared memory of a full (kBlock) block
+  size_t group_bytes = 0;  // dynamic shared memory per group
   int grid = 1, block = kBlock;
   int64_t workers = 1;
   int max_resident_groups = 1;
@@ -169,6 +173,18 @@ UpdFn update_fn(int lanes, int nr, bool det, bool atomic) {
   }
 }
 
+// Spread `workers` groups over all SMs: the smallest power-of-two block (>= one
+// warp, <= kBlock threads) that still gives every SM a block.  Workers packed
+// onto few SMs queue behind each other's row copies and REDs in the SM's LSU
+// (profiles/r01_update_kernel.md), so a low concurrency must not mean few SMs.
+void launch_shape(const asaga_ctx* ctx, int64_t workers, int* grid, int* block) {
+  const int64_t threads = workers * ctx->lanes;
+  int64_t tpb = 32;
+  while (tpb < kBlock && tpb * ctx->sms < threads) tpb *= 2;
+  *block = (int)tpb;
+  *grid = (int)((threads + tpb - 1) / tpb);
+}
+
 // Pick lanes per sample and register chunks from the row-length profile, then
 // the launch shape for the requested number of samples in flight.
 asaga_status configure_update(asaga_ctx* ctx) {
@@ -184,7 +200,12 @@ asaga_status configure_update(asaga_ctx* ctx) {
   ctx->nr = nr;
   ctx->overflow = (int)std::max<int64_t>(0, ctx->max_row - (int64_t)nr * lanes);
   const int groups_per_block = kBlock / lanes;
-  ctx->smem = (size_t)groups_per_block * (size_t)ctx->overflow * sizeof(double);
+  // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
+  // (GroupSmem in asaga_kernels.cuh)
+  const size_t group_bytes = 2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
+                             (size_t)ctx->overflow * sizeof(double);
+  ctx->group_bytes = group_bytes;
+  ctx->smem = (size_t)groups_per_block * group_bytes;
   UpdFn fn = update_fn(lanes, nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
   if (ctx->smem > 227 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
@@ -200,8 +221,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
   else if (ctx->concurrency_opt > 0) workers = std::min<int64_t>(ctx->concurrency_opt, ctx->max_resident_groups);
   else workers = ctx->max_resident_groups;
   ctx->workers = workers;
-  ctx->block = kBlock;
-  ctx->grid = (int)((workers + groups_per_block - 1) / groups_per_block);
+  launch_shape(ctx, workers, &ctx->grid, &ctx->block);
   return ASAGA_OK;
 }
 
@@ -212,10 +232,16 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->cols, nnz));
   TRY(dalloc(ctx, &ctx->y, n));
   TRY(dalloc(ctx, &ctx->vals, nnz));
-  TRY(dalloc(ctx, &ctx->st, d));
+  // Small d (every feature hot, e.g. c2's d = 54): give every feature its own
+  // 1 KiB block so hot features spread over L2 slices (2.2x at 1024 in flight,
+  // profiles/r01_update_kernel.md); larger d keeps pairs dense (S = 8 measured no gain on c3).
+  ctx->S = d <= 4096 ? 64 : 1;
+  if (const char* e = getenv("ASAGA_PAIR_STRIDE")) ctx->S = std::max(1, atoi(e));  // experiments
+  TRY(dalloc(ctx, &ctx->xa, (size_t)d * ctx->S));
+  TRY(dalloc(ctx, &ctx->D, d));
+  TRY(dalloc(ctx, &ctx->dv, nnz));
   TRY(dalloc(ctx, &ctx->alpha, n));
   TRY(dalloc(ctx, &ctx->counts, d));
-  TRY(dalloc(ctx, &ctx->xdense, d));
   TRY(dalloc(ctx, &ctx->tmp_n, n));
   TRY(dalloc(ctx, &ctx->tmp_d, d));
   TRY(dalloc(ctx, &ctx->tmp_d2, d));
@@ -278,8 +304,10 @@ asaga_status ingest(asaga_ctx* ctx, const double* data_in) {
   int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
   ingest_kernel<<<grid, kBlock, hsmem, ctx->stream>>>(ip);
   CK(ctx, cudaGetLastError());
-  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->st, d, n,
+  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->D, d, n,
                                                                         ctx->flag + 1);
+  CK(ctx, cudaGetLastError());
+  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(ctx->cols, ctx->D, nnz, ctx->dv);
   CK(ctx, cudaGetLastError());
   unsigned long long h[ERR_COUNT + 2];
   int hmax_count = 0;
@@ -443,43 +471,42 @@ asaga_status ensure_csc(asaga_ctx* ctx) {
   return ASAGA_OK;
 }
 
-// Enqueue margins (+ sigma~ if want_sig) and the objective finish for device x.
-asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, double* f_dev,
+// Enqueue margins (+ sigma~ if want_sig) and the objective finish for device x
+// (element stride xs: 1 for a dense vector, 2 for the {x, abar} pairs).
+asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, double* f_dev,
                                double* loss_sum_dev, bool want_sig, cudaStream_t s) {
   const double mean = (double)ctx->nnz / (double)ctx->n;
   double* sig = want_sig ? ctx->sig : nullptr;
   if (mean <= 8.0)
-    margin_kernel<8><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+    margin_kernel<8><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
                                                         ctx->n, sig, ctx->block_loss);
   else if (mean <= 16.0)
-    margin_kernel<16><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+    margin_kernel<16><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
                                                          ctx->n, sig, ctx->block_loss);
   else
-    margin_kernel<32><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev,
+    margin_kernel<32><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
                                                          ctx->n, sig, ctx->block_loss);
   CK(ctx, cudaGetLastError());
-  finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, ctx->d,
+  finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, xs, ctx->d,
                                              ctx->n, ctx->lambda, f_dev, loss_sum_dev);
   CK(ctx, cudaGetLastError());
   return ASAGA_OK;
 }
 
 // Enqueue sum_i sigma~_i a~_i (raw, divide=0) or the full gradient (divide=1) into g_dev.
-asaga_status enqueue_gradient(asaga_ctx* ctx, const double* x_dev, double* g_dev, int divide,
+asaga_status enqueue_gradient(asaga_ctx* ctx, const double* x_dev, int xs, double* g_dev, int divide,
                               cudaStream_t s) {
   colseg_kernel<<<grid_for(ctx, ctx->nseg * 32, kBlock), kBlock, 0, s>>>(
       ctx->seg_lo, ctx->seg_hi, ctx->nseg, ctx->csc_rows, ctx->csc_vals, ctx->sig, ctx->seg_sum);
   CK(ctx, cudaGetLastError());
   colsum_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
-      ctx->seg_ptr, ctx->seg_sum, x_dev, ctx->d, (double)ctx->n, ctx->lambda, g_dev, divide);
+      ctx->seg_ptr, ctx->seg_sum, x_dev, xs, ctx->d, (double)ctx->n, ctx->lambda, g_dev, divide);
   CK(ctx, cudaGetLastError());
   return ASAGA_OK;
 }
 
-const double* current_x(asaga_ctx* ctx, cudaStream_t s) {
-  extract_x_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->st, ctx->xdense, ctx->d);
-  return ctx->xdense;
-}
+const double* current_x(asaga_ctx* ctx) { return &ctx->xa[0].x; }  // element stride 2 * S
+int current_xs(const asaga_ctx* ctx) { return 2 * ctx->S; }
 
 asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool timed) {
   if (n_updates == 0) return ASAGA_OK;
@@ -487,7 +514,9 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.rowptr = ctx->rowptr;
   p.cols = ctx->cols;
   p.vals = ctx->vals;
-  p.st = ctx->st;
+  p.dv = ctx->dv;
+  p.xa = ctx->xa;
+  p.S = ctx->S;
   p.alpha = ctx->alpha;
   p.visits = ctx->visits;
   p.n = (uint64_t)ctx->n;
@@ -499,15 +528,20 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.T = n_updates;
   p.workers = ctx->workers;
   p.overflow = ctx->overflow;
+  p.debug_mode = 0;
+#ifdef ASAGA_TIMING
+  if (const char* m = getenv("ASAGA_DEBUG_MODE")) p.debug_mode = atoi(m);
+#endif
   UpdFn fn = update_fn(ctx->lanes, ctx->nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
-  // Fewer updates than workers: launch only what is needed.
+  // Fewer updates than workers: launch only what is needed.  The stride stays W,
+  // so the t -> worker map does not depend on the launch.
   int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
-  p.workers = ctx->workers;  // the stride stays W so the t -> worker map is launch-independent
-  const int gpb = kBlock / ctx->lanes;
-  int grid = (int)((workers + gpb - 1) / gpb);
+  int grid = 1, block = 32;
+  launch_shape(ctx, workers, &grid, &block);
+  const size_t smem = (size_t)(block / ctx->lanes) * ctx->group_bytes;
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   void* args[] = {&p};
-  CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(kBlock), args, ctx->smem, ctx->stream));
+  CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(block), args, smem, ctx->stream));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->t += n_updates;
   return ASAGA_OK;
@@ -608,7 +642,7 @@ asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
   if (n_updates == 0) return ASAGA_OK;
   TRY(enqueue_run(ctx, n_updates, seed, true));
   CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
-  nonfinite_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->st, ctx->d, ctx->flag);
+  nonfinite_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->xa, ctx->S, ctx->d, ctx->flag);
   CK(ctx, cudaGetLastError());
   int bad = 0;
   CK(ctx, cudaMemcpyAsync(&bad, ctx->flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -624,21 +658,21 @@ asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
 asaga_status asaga_objective_device(asaga_ctx* ctx, const double* x_dev, double* f_dev) {
   if (!ctx || !f_dev) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_dev is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
-  const double* x = x_dev ? x_dev : current_x(ctx, ctx->stream);
-  return enqueue_objective(ctx, x, f_dev, nullptr, false, ctx->stream);
+  if (x_dev) return enqueue_objective(ctx, x_dev, 1, f_dev, nullptr, false, ctx->stream);
+  return enqueue_objective(ctx, current_x(ctx), current_xs(ctx), f_dev, nullptr, false, ctx->stream);
 }
 
 asaga_status asaga_objective(asaga_ctx* ctx, const double* x, double* f_out) {
   if (!ctx || !f_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_out is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
-  const double* xd;
+  const double* xd = current_x(ctx);
+  int xs = current_xs(ctx);
   if (x) {
     CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, ctx->stream));
     xd = ctx->tmp_d;
-  } else {
-    xd = current_x(ctx, ctx->stream);
+    xs = 1;
   }
-  TRY(enqueue_objective(ctx, xd, ctx->scal, nullptr, false, ctx->stream));
+  TRY(enqueue_objective(ctx, xd, xs, ctx->scal, nullptr, false, ctx->stream));
   CK(ctx, cudaMemcpyAsync(f_out, ctx->scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
   return ASAGA_OK;
@@ -648,15 +682,15 @@ asaga_status asaga_full_grad(asaga_ctx* ctx, const double* x, double* g_out) {
   if (!ctx || !g_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or g_out is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
   TRY(ensure_csc(ctx));
-  const double* xd;
+  const double* xd = current_x(ctx);
+  int xs = current_xs(ctx);
   if (x) {
     CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, ctx->stream));
     xd = ctx->tmp_d;
-  } else {
-    xd = current_x(ctx, ctx->stream);
+    xs = 1;
   }
-  TRY(enqueue_objective(ctx, xd, ctx->scal, nullptr, true, ctx->stream));
-  TRY(enqueue_gradient(ctx, xd, ctx->tmp_d2, 1, ctx->stream));
+  TRY(enqueue_objective(ctx, xd, xs, ctx->scal, nullptr, true, ctx->stream));
+  TRY(enqueue_gradient(ctx, xd, xs, ctx->tmp_d2, 1, ctx->stream));
   CK(ctx, cudaMemcpyAsync(g_out, ctx->tmp_d2, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
   return ASAGA_OK;
@@ -667,8 +701,8 @@ asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double*
   CK(ctx, cudaSetDevice(ctx->device));
   TRY(ensure_csc(ctx));
   cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
-  TRY(enqueue_objective(ctx, x_dev, nullptr, out_dev + ctx->d, true, s));
-  TRY(enqueue_gradient(ctx, x_dev, out_dev, 0, s));
+  TRY(enqueue_objective(ctx, x_dev, 1, nullptr, out_dev + ctx->d, true, s));
+  TRY(enqueue_gradient(ctx, x_dev, 1, out_dev, 0, s));
   return ASAGA_OK;
 }
 
@@ -677,8 +711,8 @@ asaga_status asaga_get_state(asaga_ctx* ctx, double* x, double* alpha, double* a
   CK(ctx, cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   if (x || alpha_bar) {
-    unpack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
-        ctx->st, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, nullptr, ctx->d);
+    unpack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
+        ctx->xa, ctx->S, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
     CK(ctx, cudaGetLastError());
     if (x) CK(ctx, cudaMemcpyAsync(x, ctx->tmp_d, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
     if (alpha_bar)
@@ -703,8 +737,8 @@ asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alph
   if (alpha_bar)
     CK(ctx, cudaMemcpyAsync(ctx->tmp_d2, alpha_bar, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
   if (x || alpha_bar) {
-    pack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
-        ctx->st, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
+    pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
+        ctx->xa, ctx->S, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
     CK(ctx, cudaGetLastError());
   }
   if (alpha) {
@@ -723,12 +757,7 @@ asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double* D) {
   cudaStream_t s = ctx->stream;
   if (counts)
     CK(ctx, cudaMemcpyAsync(counts, ctx->counts, sizeof(int32_t) * ctx->d, cudaMemcpyDeviceToHost, s));
-  if (D) {
-    unpack_state_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->st, nullptr, nullptr,
-                                                                         ctx->tmp_d, ctx->d);
-    CK(ctx, cudaGetLastError());
-    CK(ctx, cudaMemcpyAsync(D, ctx->tmp_d, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
-  }
+  if (D) CK(ctx, cudaMemcpyAsync(D, ctx->D, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
   CK(ctx, cudaStreamSynchronize(s));
   return ASAGA_OK;
 }
@@ -814,6 +843,17 @@ const char* asaga_status_string(asaga_status s) {
 }
 
 int asaga_abi_version(void) { return ASAGA_ABI_VERSION; }
+
+#ifdef ASAGA_TIMING
+// Profiling build only: read and reset the per-phase cycle sums (not part of asaga.h).
+__attribute__((visibility("default"))) int asaga_debug_timing(unsigned long long* out6) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out6, g_phase_cycles, 6 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  return 0;
+}
+#endif
 
 void asaga_destroy(asaga_ctx* ctx) {
   if (!ctx) return;

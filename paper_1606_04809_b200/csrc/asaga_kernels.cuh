@@ -16,14 +16,17 @@
 
 namespace asaga {
 
-// Coordinate state, one 32-byte sector per feature v: the three values an
-// update gathers for v (x_v, abar_v, D_v) arrive in ONE 256-bit L2 load.
-struct __align__(32) Coord {
-  double x;     // iterate x_v
-  double abar;  // maintained abar_v = (1/n) sum_i alpha_i a_iv
-  double D;     // reweighting D_v = 1/p_v = n / n_v; 0 if n_v = 0
-  double pad;
-};
+// Coordinate state:
+//   xa[v*S] = {x_v, abar_v}  one 16-byte pair per feature (S = pair stride: 1, or
+//           8 / 64 for small d so every feature owns an L2 line / slice and hot
+//           features do not share a line's atomic unit): an update gathers both
+//           with ONE 128-bit L2 load (LDG.E.NA.128) and adds to both with two REDs
+//           into the same sector; abar_v = (1/n) sum_i alpha_i a_iv
+//   D[v]    reweighting 1/p_v = n / n_v
+//   dv[k]   D_{c_k} replicated per stored entry, so the row stream (cp.async,
+//           coalesced) carries D and the gather is a single wavefront per entry
+// (profiles/r01_update_kernel.md: per-entry L1TEX wavefronts, not bytes, set the
+// per-sample latency at the concurrency ASAGA converges at).
 
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11) -- own implementation (the oracle has its
@@ -54,16 +57,30 @@ __device__ __forceinline__ int64_t sample_row(uint64_t seed, uint64_t t, uint64_
 // (LDG.STRONG.GPU: L1 bypass), so a read never returns a stale L1 line of a
 // coordinate another SM has since added to -- the paper's "inconsistent read"
 // is still unsynchronised, but bounded by in-flight updates.
-__device__ __forceinline__ void ld_coord(const Coord* p, double& x, double& ab, double& D) {
-  double pad;
-  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(x), "=d"(ab), "=d"(D), "=d"(pad)
-               : "l"(p));
-  (void)pad;
-}
 __device__ __forceinline__ double ld_cg(const double* p) {
   double v;
   asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+// Gathers of shared state: weak loads that never allocate in L1 (LDG.E.NA), so
+// they always come from L2 (no stale L1 line) without the ordering cost of a
+// .STRONG.GPU load behind the warp's own outstanding REDs (profiles/r01_*.md).
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+#ifdef ASAGA_STRONG_GATHER
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#else
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+#endif
+  return v;
+}
+__device__ __forceinline__ double2 ld_na2(const double2* p) {
+  double2 v;
+#ifdef ASAGA_STRONG_GATHER
+  asm volatile("ld.global.cg.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+#else
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+#endif
   return v;
 }
 __device__ __forceinline__ void st_cg(double* p, double v) {
@@ -72,6 +89,9 @@ __device__ __forceinline__ void st_cg(double* p, double v) {
 // Atomic coordinate add (Property 3): fire-and-forget reduction at L2.
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 __device__ __forceinline__ int ld_nc_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ld_nc_f64(const double* p) { return __ldg(p); }
@@ -176,22 +196,27 @@ __global__ void __launch_bounds__(256) ingest_kernel(IngestParams p) {
 }
 
 // A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
-__global__ void profile_kernel(const int32_t* __restrict__ counts, Coord* __restrict__ st,
-                               int64_t d, int64_t n, int* __restrict__ max_count) {
+__global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa,
+                               int S, double* __restrict__ D, int64_t d, int64_t n,
+                               int* __restrict__ max_count) {
   int my = 0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int c = counts[v];
-    Coord s;
-    s.x = 0.0;
-    s.abar = 0.0;
-    s.D = c > 0 ? (double)n / (double)c : 0.0;
-    s.pad = 0.0;
-    st[v] = s;
+    xa[v * S] = make_double2(0.0, 0.0);
+    D[v] = c > 0 ? (double)n / (double)c : 0.0;
     my = max(my, c);
   }
   for (int off = 16; off > 0; off >>= 1) my = max(my, __shfl_xor_sync(0xffffffffu, my, off));
   if ((threadIdx.x & 31) == 0) atomicMax(max_count, my);
+}
+
+// A1: dv[k] = D[cols[k]] (the row stream carries D; see the layout note above).
+__global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* __restrict__ D,
+                                int64_t nnz, double* __restrict__ dv) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dv[k] = __ldg(D + cols[k]);
 }
 
 // ---------------------------------------------------------------------------
@@ -201,12 +226,16 @@ __global__ void profile_kernel(const int32_t* __restrict__ counts, Coord* __rest
 // = samples in flight).  Per sample, with folded values a~ = b a and folded
 // memory alpha~_i = b_i alpha_i (exact: b = +-1):
 //   i      = Philox(seed, t)                               line 3 (sample first)
-//   x^, abar^ on S_i via one 256-bit .cg load per v        lines 5, 7
+//   x^, abar^ on S_i (.cg loads), D (L1)                   lines 5, 7
 //   m      = sum a~_k x^_{c_k}   (group shuffle reduce)
 //   dalpha = -1/(1+exp(m)) - alpha~^_i                     lines 6, 8
-//   x_v   += -gamma (dalpha a~_k + D_v (abar^_v + lambda x^_v))   line 9, 11
+//   x_v   += -gamma (dalpha a~_k + D_v (abar^_v + lambda x^_v))   lines 9, 11
 //   abar_v += dalpha a~_k / n                              line 13
 //   alpha~_i += dalpha                                     line 12 (reading R9)
+// The samples are known in advance (counter-based sampler), so the row data of
+// sample t+W is prefetched into L1 while sample t computes, and the row bounds
+// of sample t+2W one step earlier: the HBM row fetch leaves the critical path,
+// which becomes gather (L2) -> reduce -> exp -> RED.
 // The first NR*G entries of a row keep (c, a~, q = D(abar + lambda x)) in
 // registers; longer rows stash q in shared memory and re-read c, a~ (read-only).
 // DET: one worker; a gpu-scope fence + __syncwarp between samples makes sample
@@ -215,7 +244,9 @@ struct UpdateParams {
   const int64_t* rowptr;
   const int32_t* cols;
   const double* vals;   // folded a~
-  Coord* st;
+  const double* dv;     // D_{c_k} per stored entry
+  double2* xa;          // {x_v, abar_v} at xa[v * S]
+  int S;                // pair stride
   double* alpha;        // folded alpha~
   int32_t* visits;      // NULL unless record_samples
   uint64_t n;
@@ -223,100 +254,199 @@ struct UpdateParams {
   uint64_t seed, t0, T;
   int64_t workers;
   int overflow;         // shared-memory q slots per group (>= max_row - NR*G, or 0)
+  int debug_mode;       // profiling build only: bit0 skip the scatter, bit1 skip exp/div
 };
 
+// cp.async (LDGSTS) helpers: the next sample's row is copied global -> shared
+// while the current sample computes.  Lane g copies and later reads only its own
+// entries (k = lo + j*G + g), so no cross-lane barrier is needed.
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Shared memory per group: 2 stages x P = NR*G row entries (fp64 value, fp64 D,
+// int32 index), then `overflow` fp64 q slots for rows longer than P.
+template <int G, int NR>
+struct GroupSmem {
+  static constexpr int P = NR * G;
+  static constexpr size_t stage_bytes = (size_t)P * (2 * sizeof(double) + sizeof(int32_t));
+  static __host__ __device__ size_t bytes(int overflow) {
+    return 2 * stage_bytes + (size_t)overflow * sizeof(double);
+  }
+};
+
+template <int G, int NR>
+__device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, const int32_t* cols,
+                                               const double* vals, const double* dv, int64_t lo,
+                                               int64_t hi, int g) {
+  constexpr int P = NR * G;
+  double* sv = reinterpret_cast<double*>(base + stage * GroupSmem<G, NR>::stage_bytes);
+  double* sd = sv + P;
+  int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if (lo + j * G >= hi) break;  // group-uniform: no predicated-off chunks
+    const int64_t k = lo + j * G + g;
+    if (k < hi) {
+      cp_async4(sc + j * G + g, cols + k);
+      cp_async8(sv + j * G + g, vals + k);
+      cp_async8(sd + j * G + g, dv + k);
+    }
+  }
+  cp_async_commit();
+}
+
+#ifdef ASAGA_TIMING
+// Profiling build only (tools/timing_build.py): per-phase SM-cycle sums of group
+// leaders: [0] row wait, [1] gathers+dot, [2] reduce+exp, [3] scatter issue,
+// [4] loop tail, [5] iterations.
+__device__ unsigned long long g_phase_cycles[8];
+#define TMARK(k)                                     \
+  do {                                               \
+    long long now_ = clock64();                      \
+    ph[k] += (unsigned long long)(now_ - tprev);     \
+    tprev = now_;                                    \
+  } while (0)
+#else
+#define TMARK(k) \
+  do {           \
+  } while (0)
+#endif
+
 template <int G, int NR, bool DET, bool ATOMIC>
-__global__ void __launch_bounds__(256) asaga_update_kernel(UpdateParams p) {
-  extern __shared__ double q_stash[];
+__global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
+#ifdef ASAGA_TIMING
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+#endif
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int P = NR * G;
   const int lane = threadIdx.x & 31;
   const int g = lane & (G - 1);
   const unsigned gmask =
       (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   if (w >= p.workers) return;
-  double* qs = q_stash + (size_t)(threadIdx.x / G) * (size_t)p.overflow;
+  unsigned char* gbase = smem_raw + (size_t)(threadIdx.x / G) * GroupSmem<G, NR>::bytes(p.overflow);
+  double* qs = reinterpret_cast<double*>(gbase + 2 * GroupSmem<G, NR>::stage_bytes);
 
   const uint64_t tend = p.t0 + p.T;
   uint64_t t = p.t0 + (uint64_t)w;
   if (t >= tend) return;
   const uint64_t W = (uint64_t)p.workers;
+  // prologue: current row bounds + its copy; next row bounds; next-next index
   int64_t i = sample_row(p.seed, t, p.n);
   int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
+  int stage = 0;
+  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, lo, hi, g);
+  int64_t in1 = 0, lo1 = 0, hi1 = 0, in2 = 0;
+  if (t + W < tend) {
+    in1 = sample_row(p.seed, t + W, p.n);
+    lo1 = __ldg(&p.rowptr[in1]);
+    hi1 = __ldg(&p.rowptr[in1 + 1]);
+  }
+  if (t + 2 * W < tend) in2 = sample_row(p.seed, t + 2 * W, p.n);
 
   while (true) {
-    // ---- pass 1: row entries, gathers of (x, abar, D), dot product
-    int cc[NR];
-    double aa[NR], qq[NR];
+    // ---- pass 1: row entries (shared memory), gathers, dot product
+    cp_async_wait_all();
+    TMARK(0);
+    const double* sv = reinterpret_cast<const double*>(gbase + stage * GroupSmem<G, NR>::stage_bytes);
+    const double* sd = sv + P;
+    const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
+    // gathers of x^, abar^ and D for every resident chunk are issued before any use
+    double qq[NR];
+    double2 xb[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
+      if (lo + j * G >= hi) break;  // group-uniform
       const int64_t k = lo + j * G + g;
-      if (k < hi) {
-        cc[j] = ld_nc_i32(p.cols + k);
-        aa[j] = ld_nc_f64(p.vals + k);
-      }
+      if (k < hi) xb[j] = ld_na2(p.xa + (int64_t)sc[j * G + g] * p.S);
+    }
+    const double ai = ld_na(p.alpha + i);
+    // ---- look-ahead (read-only data): copy row t+W, load bounds of t+2W
+    const bool has1 = t + W < tend, has2 = t + 2 * W < tend;
+    if (has1) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
+    int64_t lo2 = 0, hi2 = 0;
+    if (has2) {
+      lo2 = __ldg(&p.rowptr[in2]);
+      hi2 = __ldg(&p.rowptr[in2 + 1]);
     }
     double dot = 0.0;
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
+      if (lo + j * G >= hi) break;  // group-uniform
       const int64_t k = lo + j * G + g;
       if (k < hi) {
-        double x, ab, D;
-        ld_coord(p.st + cc[j], x, ab, D);
-        dot = fma(aa[j], x, dot);
-        qq[j] = D * fma(p.lambda_, x, ab);
+        dot = fma(sv[j * G + g], xb[j].x, dot);
+        qq[j] = sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
       }
     }
-    for (int64_t k = lo + NR * G + g; k < hi; k += G) {  // long rows only
+    for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
-      double x, ab, D;
-      ld_coord(p.st + c, x, ab, D);
-      dot = fma(a, x, dot);
-      qs[k - lo - NR * G] = D * fma(p.lambda_, x, ab);
+      const double2 v = ld_na2(p.xa + (int64_t)c * p.S);
+      dot = fma(a, v.x, dot);
+      qs[k - lo - P] = ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
     }
-    const double ai = ld_cg(p.alpha + i);
-    // ---- prefetch the next sample's row bounds (read-only data)
-    const uint64_t tn = t + W;
-    int64_t in_ = 0, lon = 0, hin = 0;
-    if (tn < tend) {
-      in_ = sample_row(p.seed, tn, p.n);
-      lon = __ldg(&p.rowptr[in_]);
-      hin = __ldg(&p.rowptr[in_ + 1]);
-    }
+    TMARK(1);
     // ---- scalar derivative (folded logistic) and memory difference
     dot = group_sum<G>(dot, gmask);
+#ifdef ASAGA_TIMING
+    const double sig = (p.debug_mode & 2) ? -0.5 + 0.0 * dot : -1.0 / (1.0 + exp(dot));
+#else
     const double sig = -1.0 / (1.0 + exp(dot));
+#endif
     const double da = sig - ai;
     const double ngam = -p.gamma;
-    // ---- pass 2: unlocked scatter
+    TMARK(2);
+#ifdef ASAGA_TIMING
+    if (!(p.debug_mode & 1)) {
+#endif
+    // ---- pass 2: unlocked scatter (Property 3: atomic adds, no locks); row entries
+    //      are re-read from the stage buffer, which is only overwritten next iteration
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
+      if (lo + j * G >= hi) break;  // group-uniform
       const int64_t k = lo + j * G + g;
       if (k < hi) {
-        const double u = fma(da, aa[j], qq[j]);
-        Coord* s = p.st + cc[j];
+        const int c = sc[j * G + g];
+        const double a = sv[j * G + g];
+        const double u = fma(da, a, qq[j]);
+        double* xv = &p.xa[(int64_t)c * p.S].x;
         if (ATOMIC) {
-          red_add(&s->x, ngam * u);
-          red_add(&s->abar, da * aa[j] * p.inv_n);
+          red_add(xv, ngam * u);
+          red_add(xv + 1, da * a * p.inv_n);
         } else {
-          st_cg(&s->x, ld_cg(&s->x) + ngam * u);
-          st_cg(&s->abar, ld_cg(&s->abar) + da * aa[j] * p.inv_n);
+          st_cg(xv, ld_cg(xv) + ngam * u);
+          st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
         }
       }
     }
-    for (int64_t k = lo + NR * G + g; k < hi; k += G) {
+    for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
-      const double u = fma(da, a, qs[k - lo - NR * G]);
-      Coord* s = p.st + c;
+      const double u = fma(da, a, qs[k - lo - P]);
+      double* xv = &p.xa[(int64_t)c * p.S].x;
       if (ATOMIC) {
-        red_add(&s->x, ngam * u);
-        red_add(&s->abar, da * a * p.inv_n);
+        red_add(xv, ngam * u);
+        red_add(xv + 1, da * a * p.inv_n);
       } else {
-        st_cg(&s->x, ld_cg(&s->x) + ngam * u);
-        st_cg(&s->abar, ld_cg(&s->abar) + da * a * p.inv_n);
+        st_cg(xv, ld_cg(xv) + ngam * u);
+        st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
       }
     }
+#ifdef ASAGA_TIMING
+    }
+#endif
+    TMARK(3);
     if (g == 0) {
       if (ATOMIC) red_add(p.alpha + i, da);
       else st_cg(p.alpha + i, ai + da);
@@ -326,30 +456,33 @@ __global__ void __launch_bounds__(256) asaga_update_kernel(UpdateParams p) {
       __threadfence();
       __syncwarp(gmask);
     }
-    if (tn >= tend) break;
-    t = tn;
-    i = in_;
-    lo = lon;
-    hi = hin;
+#ifdef ASAGA_TIMING
+    ph[5] += 1;
+#endif
+    TMARK(4);
+    if (!has1) break;
+    t += W;
+    i = in1; lo = lo1; hi = hi1;
+    in1 = in2; lo1 = lo2; hi1 = hi2;
+    if (t + 2 * W < tend) in2 = sample_row(p.seed, t + 2 * W, p.n);
+    stage ^= 1;
   }
+  cp_async_wait_all();
+#ifdef ASAGA_TIMING
+  if (g == 0)
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_phase_cycles[k], ph[k]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
 // A9: objective / gradient (Section 4.1).  Deterministic: fixed grid, fixed
 // per-group row order, fixed-order block partials.
-__global__ void extract_x_kernel(const Coord* __restrict__ st, double* __restrict__ x,
-                                 int64_t d) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
-       v += (int64_t)gridDim.x * blockDim.x)
-    x[v] = st[v].x;
-}
-
 // Per row: m_i = a~_i . x, loss_i = softplus(-m_i) = log(1+exp(-b_i a_i.x)),
 // sigma~_i = -1/(1+exp(m_i)) (so sigma_i a_i = sigma~_i a~_i).
 template <int G>
 __global__ void __launch_bounds__(256)
 margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-              const double* __restrict__ vals, const double* __restrict__ x, int64_t n,
+              const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
               double* __restrict__ sig, double* __restrict__ block_loss) {
   __shared__ double grp_loss[256 / G];
   const int lane = threadIdx.x & 31, g = lane & (G - 1);
@@ -361,7 +494,7 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / G) + gib; i < n; i += groups) {
     const int64_t lo = rowptr[i], hi = rowptr[i + 1];
     double m = 0.0;
-    for (int64_t k = lo + g; k < hi; k += G) m = fma(vals[k], __ldg(x + cols[k]), m);
+    for (int64_t k = lo + g; k < hi; k += G) m = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m);
     m = group_sum<G>(m, gmask);
     // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
     const double loss = fmax(-m, 0.0) + log1p(exp(-fabs(m)));
@@ -380,12 +513,12 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
 // Single block: f = (sum block_loss) / n + lambda/2 ||x||^2; also raw loss sum.
 __global__ void __launch_bounds__(1024)
 finish_objective_kernel(const double* __restrict__ block_loss, int nblocks,
-                        const double* __restrict__ x, int64_t d, int64_t n, double lambda_,
+                        const double* __restrict__ x, int xs, int64_t d, int64_t n, double lambda_,
                         double* __restrict__ f_out, double* __restrict__ loss_sum_out) {
   __shared__ double s_loss[1024], s_sq[1024];
   double a = 0.0, b = 0.0;
   for (int j = threadIdx.x; j < nblocks; j += blockDim.x) a += block_loss[j];
-  for (int64_t v = threadIdx.x; v < d; v += blockDim.x) b = fma(x[v], x[v], b);
+  for (int64_t v = threadIdx.x; v < d; v += blockDim.x) b = fma(x[xs * v], x[xs * v], b);
   s_loss[threadIdx.x] = a;
   s_sq[threadIdx.x] = b;
   __syncthreads();
@@ -423,13 +556,13 @@ colseg_kernel(const int64_t* __restrict__ seg_lo, const int64_t* __restrict__ se
 // g_v = scale * (sum of v's segments, in order) + lambda x_v.
 __global__ void colsum_kernel(const int64_t* __restrict__ seg_ptr,
                               const double* __restrict__ seg_sum, const double* __restrict__ x,
-                              int64_t d, double inv_scale_div, double lambda_,
+                              int xs, int64_t d, double inv_scale_div, double lambda_,
                               double* __restrict__ g, int divide) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int64_t j = seg_ptr[v]; j < seg_ptr[v + 1]; ++j) s += seg_sum[j];
-    g[v] = divide ? s / inv_scale_div + lambda_ * x[v] : s;
+    g[v] = divide ? s / inv_scale_div + lambda_ * x[xs * v] : s;
   }
 }
 
@@ -484,11 +617,11 @@ __global__ void segfill_kernel(const int64_t* __restrict__ colptr,
 }
 
 // K5 divergence guard: flag if any x_v is not finite.
-__global__ void nonfinite_kernel(const Coord* __restrict__ st, int64_t d, int* __restrict__ flag) {
+__global__ void nonfinite_kernel(const double2* __restrict__ xa, int S, int64_t d, int* __restrict__ flag) {
   bool bad = false;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x)
-    bad |= !isfinite(st[v].x);
+    bad |= !isfinite(xa[v * S].x);
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
@@ -507,22 +640,21 @@ __global__ void fold_alpha_kernel(const double* __restrict__ in, const double* _
     out[i] = y[i] * in[i];
 }
 
-__global__ void pack_state_kernel(Coord* __restrict__ st, const double* __restrict__ x,
-                                  const double* __restrict__ ab, int64_t d) {
+__global__ void unpack_xa_kernel(const double2* __restrict__ xa, int S, double* __restrict__ x,
+                                 double* __restrict__ ab, int64_t d) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
-    if (x) st[v].x = x[v];
-    if (ab) st[v].abar = ab[v];
+    if (x) x[v] = xa[v * S].x;
+    if (ab) ab[v] = xa[v * S].y;
   }
 }
 
-__global__ void unpack_state_kernel(const Coord* __restrict__ st, double* __restrict__ x,
-                                    double* __restrict__ ab, double* __restrict__ D, int64_t d) {
+__global__ void pack_xa_kernel(double2* __restrict__ xa, int S, const double* __restrict__ x,
+                               const double* __restrict__ ab, int64_t d) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
-    if (x) x[v] = st[v].x;
-    if (ab) ab[v] = st[v].abar;
-    if (D) D[v] = st[v].D;
+    if (x) xa[v * S].x = x[v];
+    if (ab) xa[v * S].y = ab[v];
   }
 }
 

@@ -55,10 +55,11 @@ def test_library_is_sm100a(libpath):
     assert "sm_100a" in out
 
 
-def test_update_kernel_sass_uses_l2_atomics_and_256bit_gathers(libpath):
+def test_update_kernel_sass_uses_l2_atomics_and_l1_bypass(libpath):
     sass = subprocess.run(["cuobjdump", "-sass", libpath], capture_output=True, text=True).stdout
     assert "REDG.E.ADD.F64.RN.STRONG.GPU" in sass  # red.global.add.f64 coordinate adds
-    assert "LDG.E.ENL2.256.STRONG.GPU" in sass  # one 32-byte {x, abar, D} gather per entry
+    assert "LDG.E.NA.128" in sass  # one L1-bypassing 16-byte {x, abar} gather per entry
+    assert "LDGSTS" in sass  # cp.async copy of the next sample's row into shared memory
     assert "HMMA" not in sass and "UTCHMMA" not in sass  # no tensor-core path here
 
 

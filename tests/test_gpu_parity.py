@@ -358,3 +358,20 @@ def test_errors():
     with pytest.raises(E) as ei:
         d.run(2000, SEED)
     assert ei.value.name == "ASAGA_E_DIVERGED"
+
+
+@gpu
+def test_sharded_objective_single_rank_cuda():
+    """ShardedObjective with the CUDA partial (no process group: one rank owns all rows)."""
+    import torch
+
+    from paper_1606_04809_b200.sharded import ShardedObjective
+
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=20_000)
+    a = m.Asaga.from_problem(p, 1.0)
+    obj = ShardedObjective(p.n, p.d, p.lam, shard_ctx=a, device=torch.device("cuda", 0))
+    x = np.random.default_rng(9).standard_normal(p.d)
+    f, g = obj(torch.from_numpy(x).cuda())
+    assert f == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+    assert rel(g.cpu().numpy(), oracle.full_grad(p, p.y, p.lam, x)) <= 1e-10

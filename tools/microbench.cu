@@ -77,6 +77,37 @@ __global__ void k_red_same(double* tab, uint32_t k, uint32_t stride, int iters) 
   }
 }
 
+// one address per warp: lane 0 loads (.cg) then REDs -- the per-line service rate
+// of the update kernel's hot-feature pattern (1 load + 1 RED per update per line)
+__global__ void k_ldred_hot(double* tab, uint32_t k, uint32_t stride, int iters, int do_load) {
+  const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if ((threadIdx.x & 31) != 0) return;
+  double acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    double* a = tab + (size_t)((wid + it) % k) * stride;
+    double v = 0;
+    if (do_load) asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(a));
+    acc += v;
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(1.0 + acc * 0.0) : "memory");
+  }
+}
+
+// the update kernel's exact hot-feature pattern: one 16-byte {x, abar} .na load
+// + two REDs (x, abar) into that pair, per "update", k pairs 1 KiB apart
+__global__ void k_pair_hot(double* tab, uint32_t k, int iters) {
+  const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if ((threadIdx.x & 31) != 0) return;
+  double acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    double* a = tab + (size_t)((wid + it) % k) * 128;
+    double v0, v1;
+    asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v0), "=d"(v1) : "l"(a));
+    acc += v0 + v1;
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(1.0 + acc * 0.0) : "memory");
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a + 1), "d"(1.0 + acc * 0.0) : "memory");
+  }
+}
+
 __global__ void k_red_list(double* tab, const uint32_t* __restrict__ list, uint64_t m, uint32_t stride) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x)
     asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)__ldg(list + j) * stride), "d"(1.0) : "memory");
@@ -223,6 +254,42 @@ int main(int argc, char** argv) {
         first = 0;
         CK(cudaFree(tab));
       }
+    }
+    js += "}";
+  }
+  // M4b single-lane load+RED per address (request rate per hot line)
+  {
+    js += ", \"hot_line\": {";
+    int first = 1;
+    for (int do_load : {0, 1}) {
+      for (uint32_t k : {1u, 10u}) {
+        double* tab;
+        CK(cudaMalloc(&tab, (size_t)k * 128 * 8));
+        CK(cudaMemset(tab, 0, (size_t)k * 128 * 8));
+        const int blocks = sms * 8, threads = 256, iters = 32;
+        const double g = (double)blocks * (threads / 32) * iters;
+        float ms = best_ms([&] { k_ldred_hot<<<blocks, threads>>>(tab, k, 128, iters, do_load); });
+        snprintf(buf, sizeof buf, "%s\"%s_k%u\": {\"reds_per_s\": %.4g, \"per_line\": %.4g}", first ? "" : ", ",
+                 do_load ? "ld_red" : "red", k, g / ms * 1e3, g / ms * 1e3 / k);
+        js += buf;
+        first = 0;
+        CK(cudaFree(tab));
+      }
+    }
+    js += "}, \"hot_pair\": {";
+    first = 1;
+    for (uint32_t k : {1u, 10u}) {
+      double* tab;
+      CK(cudaMalloc(&tab, (size_t)k * 128 * 8));
+      CK(cudaMemset(tab, 0, (size_t)k * 128 * 8));
+      const int blocks = sms * 8, threads = 256, iters = 32;
+      const double g = (double)blocks * (threads / 32) * iters;
+      float ms = best_ms([&] { k_pair_hot<<<blocks, threads>>>(tab, k, iters); });
+      snprintf(buf, sizeof buf, "%s\"k%u\": {\"updates_per_s_per_pair\": %.4g}", first ? "" : ", ", k,
+               g / ms * 1e3 / k);
+      js += buf;
+      first = 0;
+      CK(cudaFree(tab));
     }
     js += "}";
   }

@@ -1,0 +1,60 @@
+"""Per-phase cycle breakdown of the update kernel (clock64-instrumented build).
+
+    python tools/phase_timing.py c3 --conc 64,512
+Phases per sample (group leaders): row wait | gathers+dot | reduce+exp | scatter issue | tail.
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg")
+    ap.add_argument("--conc", default="64,512")
+    ap.add_argument("--gscale", type=float, default=0.25)
+    ap.add_argument("--atomic", type=int, default=1)
+    ap.add_argument("--lanes", type=int, default=0)
+    args = ap.parse_args()
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_asaga_build", os.path.join(ROOT, "paper_1606_04809_b200", "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)
+    os.environ["ASAGA_LIB"] = _build.build(timing=True)  # before the package loads its .so
+    import torch
+
+    import datagen
+    from paper_1606_04809_b200 import Asaga, asaga
+
+    lib = asaga.lib()
+    lib.asaga_debug_timing.restype = ctypes.c_int
+    lib.asaga_debug_timing.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    p = datagen.make(args.cfg)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0,
+              atomic=bool(args.atomic), lanes_per_sample=args.lanes)
+    a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
+    buf = (ctypes.c_ulonglong * 6)()
+    names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail"]
+    for W in [int(c) for c in args.conc.split(",")]:
+        a.set_concurrency(W)
+        a.run(p.n, 1)
+        lib.asaga_debug_timing(buf)
+        a.run(p.n, 1)
+        lib.asaga_debug_timing(buf)
+        it = max(buf[5], 1)
+        st = a.stats()
+        cyc = [buf[k] / it for k in range(5)]
+        print(f"{args.cfg} G={st['lanes_per_sample']} atomic={args.atomic} W={st['concurrency']} upd/s={p.n / st['last_run_ms'] * 1e3:.4g} "
+              f"cycles/sample total={sum(cyc):.0f}: " + " ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc)))
+
+
+if __name__ == "__main__":
+    main()

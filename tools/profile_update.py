@@ -1,0 +1,39 @@
+"""Drive the update kernel for ncu: one warm-up launch, then one measured launch.
+
+    ncu --set full -k regex:asaga_update -s 1 -c 1 python tools/profile_update.py c3 --conc 512
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg")
+    ap.add_argument("--conc", type=int, default=0)
+    ap.add_argument("--gscale", type=float, default=0.25)
+    ap.add_argument("--updates", type=int, default=0, help="default: one epoch")
+    args = ap.parse_args()
+    import torch
+    from paper_1606_04809_b200 import Asaga
+
+    p = datagen.make(args.cfg)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc)
+    a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
+    T = args.updates or p.n
+    a.run(T, datagen.SAMPLE_SEED)  # warm-up launch
+    a.run(T, datagen.SAMPLE_SEED)  # profiled launch
+    st = a.stats()
+    print(f"{args.cfg} W={st['concurrency']} updates={T} ms={st['last_run_ms']:.3f} "
+          f"upd/s={T / st['last_run_ms'] * 1e3:.4g}")
+
+
+if __name__ == "__main__":
+    main()
