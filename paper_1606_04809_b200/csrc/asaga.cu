@@ -245,7 +245,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->tmp_n, n));
   TRY(dalloc(ctx, &ctx->tmp_d, d));
   TRY(dalloc(ctx, &ctx->tmp_d2, d));
-  ctx->obj_blocks = ctx->sms * 4;
+  ctx->obj_blocks = ctx->sms * 6;  // 48 resident warps per SM at 40 registers (fixed: deterministic sums)
   TRY(dalloc(ctx, &ctx->block_loss, ctx->obj_blocks));
   TRY(dalloc(ctx, &ctx->scal, 4));
   TRY(dalloc(ctx, &ctx->flag, 4));
@@ -258,7 +258,8 @@ asaga_status alloc_state(asaga_ctx* ctx) {
 // buffers, values in data_in (the caller's device array, or ctx->vals itself
 // after a host copy -- the fold is elementwise, so in place is safe).  Resets
 // the state to x = 0, alpha = 0, abar = 0, t = 0 (reading R1).
-asaga_status ingest(asaga_ctx* ctx, const double* data_in) {
+asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
+                    const double* data_in, const double* y_in) {
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
@@ -281,10 +282,13 @@ asaga_status ingest(asaga_ctx* ctx, const double* data_in) {
   }
 
   IngestParams ip;
-  ip.indptr = ctx->rowptr;
-  ip.indices = ctx->cols;
+  ip.indptr = indptr_in;
+  ip.indices = indices_in;
   ip.data = data_in;
-  ip.y = ctx->y;
+  ip.y = y_in;
+  ip.rowptr_out = ctx->rowptr;
+  ip.cols_out = ctx->cols;
+  ip.y_out = ctx->y;
   ip.vals = ctx->vals;
   ip.counts = ctx->counts;
   ip.err_row = scratch;
@@ -295,15 +299,19 @@ asaga_status ingest(asaga_ctx* ctx, const double* data_in) {
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
   const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 0;
-  CK(ctx, cudaFuncSetAttribute((const void*)ingest_kernel,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
+  const double mean = n ? (double)nnz / (double)n : 1.0;
+  const void* kfn = mean <= 8.0 ? (const void*)ingest_kernel<8>
+                    : mean <= 16.0 ? (const void*)ingest_kernel<16> : (const void*)ingest_kernel<32>;
+  const int gl = mean <= 8.0 ? 8 : (mean <= 16.0 ? 16 : 32);
+  constexpr int kIngestBlock = 1024;
+  CK(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
   int per_sm = 1;
-  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)ingest_kernel, kBlock, hsmem));
+  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kIngestBlock, hsmem));
   per_sm = std::max(per_sm, 1);
-  int64_t want = (n + (kBlock / 32) - 1) / (kBlock / 32);
-  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
-  ingest_kernel<<<grid, kBlock, hsmem, ctx->stream>>>(ip);
-  CK(ctx, cudaGetLastError());
+  const int64_t want = (n + (kIngestBlock / gl) - 1) / (kIngestBlock / gl);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
+  void* iargs[] = {&ip};
+  CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
   profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->D, d, n,
                                                                         ctx->flag + 1);
   CK(ctx, cudaGetLastError());
@@ -608,7 +616,7 @@ asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double*
   CK(ctx, cudaMemcpyAsync(ctx->vals, A->data, sizeof(double) * ctx->nnz, cudaMemcpyHostToDevice,
                           ctx->stream));
   CK(ctx, cudaMemcpyAsync(ctx->y, y, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
-  return ingest(ctx, ctx->vals);
+  return ingest(ctx, ctx->rowptr, ctx->cols, ctx->vals, ctx->y);
 }
 
 asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
@@ -622,12 +630,8 @@ asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A, const 
   if (ends[0] != 0 || ends[1] != ctx->nnz)
     return fail(ctx, ASAGA_E_BAD_CSR, "indptr[0] must be 0 and indptr[n] must be nnz (got %lld and %lld, nnz=%lld)",
                 (long long)ends[0], (long long)ends[1], (long long)ctx->nnz);
-  CK(ctx, cudaMemcpyAsync(ctx->rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1),
-                          cudaMemcpyDeviceToDevice, ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyDeviceToDevice,
-                          ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->y, y, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
-  return ingest(ctx, A->data);
+  // the ingest pass itself copies rowptr / cols / y into the context (one read each)
+  return ingest(ctx, A->indptr, A->indices, A->data, y);
 }
 
 asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {

@@ -109,11 +109,14 @@ enum : int { ERR_ROW_BOUNDS = 0, ERR_EMPTY_ROW, ERR_INDEX_RANGE, ERR_INDEX_ORDER
              ERR_NONFINITE, ERR_LABEL, ERR_COUNT };
 
 struct IngestParams {
-  const int64_t* indptr;  // n+1
+  const int64_t* indptr;  // n+1   (caller's array, or the context's after a host copy)
   const int32_t* indices; // nnz
   const double* data;     // nnz (unfolded)
   const double* y;        // n
-  double* vals;           // out: folded values b_i a_ik
+  int64_t* rowptr_out;    // the context's own copies (may alias the inputs: in place)
+  int32_t* cols_out;
+  double* y_out;
+  double* vals;           // out: folded values b_i a_ik (may alias data)
   int32_t* counts;        // out (pre-zeroed): n_v
   unsigned long long* err_row;   // [ERR_COUNT], pre-set to ULLONG_MAX; atomicMin(row)
   unsigned long long* max_sq;    // bits of max_i ||a_i||^2 (>= 0 doubles order as u64)
@@ -122,68 +125,95 @@ struct IngestParams {
   int smem_hist;          // 1: per-block shared histogram of all d columns
 };
 
-__global__ void __launch_bounds__(256) ingest_kernel(IngestParams p) {
+// One pass over the caller's CSR: validate (errors carry the first bad row), copy
+// rowptr / cols / y into the context, fold b_i into the values, count n_v
+// (shared-memory histogram when d fits, flushed once per block), max ||a_i||^2
+// and the longest row.  Rows go to G-lane groups; each element is read once (the
+// previous index for the order check comes from a shuffle).
+template <int G>
+__global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
   extern __shared__ int32_t hist[];
-  __shared__ double warp_max[8];
-  __shared__ long long warp_len[8];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  __shared__ double blk_max[32];
+  __shared__ long long blk_len[32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
   if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
     __syncthreads();
   }
   double my_max = 0.0;
-  int64_t my_len = 0;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; i < p.n; i += warps) {
+  long long my_len = 0;
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; i < p.n; i += groups) {
     const int64_t lo = p.indptr[i], hi = p.indptr[i + 1];
+    if (g == 0) {
+      p.rowptr_out[i] = lo;
+      if (i == p.n - 1) p.rowptr_out[p.n] = hi;
+    }
     if (lo < 0 || hi > p.nnz || hi < lo) {
-      if (lane == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
+      if (g == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
       continue;
     }
     if (hi == lo) {
-      if (lane == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
+      if (g == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
       continue;
     }
-    my_len = max(my_len, hi - lo);
+    my_len = max(my_len, (long long)(hi - lo));
     const double b = p.y[i];
-    if (b != 1.0 && b != -1.0) {
-      if (lane == 0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
+    if (g == 0) {
+      p.y_out[i] = b;
+      if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
     }
     double sq = 0.0;
     bool bad_range = false, bad_order = false, bad_val = false;
-    for (int64_t k = lo + lane; k < hi; k += 32) {
-      const int32_t c = p.indices[k];
-      const double v = p.data[k];
-      bad_range |= (c < 0) || ((int64_t)c >= p.d);
-      if (k > lo) bad_order |= (p.indices[k - 1] >= c);
-      bad_val |= !isfinite(v);
-      p.vals[k] = b * v;
-      sq = fma(v, v, sq);
-      if (c >= 0 && (int64_t)c < p.d) {
-        if (p.smem_hist) atomicAdd(&hist[c], 1);
-        else atomicAdd(&p.counts[c], 1);
+    int carry = -1;  // last index of the previous chunk (group-uniform)
+    for (int64_t base = lo; base < hi; base += G) {
+      const int64_t k = base + g;
+      const bool in = k < hi;
+      const int32_t c = in ? p.indices[k] : INT32_MAX;
+      const double v = in ? p.data[k] : 0.0;
+      int prev = __shfl_up_sync(gmask, c, 1, G);
+      if (g == 0) prev = carry;
+      if (in) {
+        bad_range |= (c < 0) || ((int64_t)c >= p.d);
+        bad_order |= (base + g > lo) && (prev >= c);
+        bad_val |= !isfinite(v);
+        p.cols_out[k] = c;
+        p.vals[k] = b * v;
+        sq = fma(v, v, sq);
+        if (c >= 0 && (int64_t)c < p.d) {
+          if (p.smem_hist) atomicAdd(&hist[c], 1);
+          else atomicAdd(&p.counts[c], 1);
+        }
       }
+      carry = __shfl_sync(gmask, c, G - 1, G);
     }
-    if (__any_sync(0xffffffffu, bad_range) && lane == 0)
+    if (__any_sync(gmask, bad_range) && g == 0)
       atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
-    if (__any_sync(0xffffffffu, bad_order) && lane == 0)
+    if (__any_sync(gmask, bad_order) && g == 0)
       atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
-    if (__any_sync(0xffffffffu, bad_val) && lane == 0)
+    if (__any_sync(gmask, bad_val) && g == 0)
       atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
-    sq = group_sum<32>(sq, 0xffffffffu);
+    sq = group_sum<G>(sq, gmask);
     my_max = fmax(my_max, sq);
   }
+  // block maxima (warp shuffles, then one atomic per block)
+  for (int off = 16; off > 0; off >>= 1) {
+    my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
+    my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
+  }
   if (lane == 0) {
-    warp_max[wib] = my_max;
-    warp_len[wib] = my_len;
+    blk_max[wib] = my_max;
+    blk_len[wib] = my_len;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 0.0;
     long long L = 0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      m = fmax(m, warp_max[w]);
-      L = max(L, warp_len[w]);
+      m = fmax(m, blk_max[w]);
+      L = max(L, blk_len[w]);
     }
     atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
     atomicMax(p.max_len, (unsigned long long)L);
