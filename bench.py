@@ -35,10 +35,11 @@ sys.path.insert(0, ROOT)
 
 import datagen  # noqa: E402
 
-# Convergent operating points (W samples in flight, gamma scale vs 1/(3L)) from
-# tools/sweep.py on B200 (profiles/r01_operating_point.md): the fastest
-# time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
-OPERATING_POINT = {"c1": (16, 1.0), "c2": (1024, 0.125), "c3": (256, 0.35), "c4": (256, 0.25)}
+# Convergent operating points (W samples in flight, gamma scale vs 1/(3L), bulk-scatter
+# feature frequency) from tools/sweep.py on B200 (profiles/r01_operating_point.md):
+# the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
+OPERATING_POINT = {"c1": (16, 1.0, 0.0), "c2": (1024, 0.125, 0.5), "c3": (256, 0.35, 0.0),
+                   "c4": (256, 0.25, 0.0)}
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -220,14 +221,15 @@ def main():
     from paper_1606_04809_b200 import Asaga
 
     p = datagen.make(args.workload)
-    W0, gs0 = OPERATING_POINT[args.workload]
+    W0, gs0, bulk = OPERATING_POINT[args.workload]
     W = args.concurrency if args.concurrency is not None else W0
     gscale = args.gamma_scale if args.gamma_scale is not None else gs0
     lam = p.lam * (10.0 ** (-rank))  # rank 0: lambda = 1/n (the BASELINE config)
     dev = torch.device("cuda", local)
     t = lambda arr: torch.from_numpy(arr).to(dev)
     indptr, indices, data, y = t(p.indptr), t(p.indices), t(p.data), t(p.y)
-    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local)
+    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local,
+              bulk_scatter_min_freq=bulk)
     L = a.stats()["L"]
     gamma = gscale / (3.0 * L)
     a.set_gamma(gamma)
@@ -320,6 +322,7 @@ def main():
             "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz,
                        "samples_in_flight": st["concurrency"], "lanes_per_sample": st["lanes_per_sample"],
                        "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale, "lambda": "10^-rank / n",
+                       "bulk_scatter_min_freq": bulk,
                        "l2_flush": "512 MiB write between steps (outside the timed events)",
                        "parallelism": f"{world} independent lambda-sweep instances" if world > 1 else "1 GPU"},
             "breakdown_ms": {"ingest_A0_A1": float(np.mean(ing_ms)), "updates_A2_A8": float(np.mean(upd_ms)),

@@ -84,6 +84,12 @@ typedef struct {
   int record_samples;    /* 1: count visits per row (int32[n]) to check the sample stream */
   void* stream;          /* cudaStream_t to run on (e.g. torch's current stream);
                             NULL = a stream owned by the context */
+  double bulk_scatter_min_freq; /* features present in at least this fraction of rows
+                            (p_v >= it) are updated with one TMA bulk 16-byte reduction of
+                            the {x_v, abar_v} pair instead of two red.global.add.f64: one L2
+                            operation on the feature's line instead of two (the hot line is
+                            the throughput bound), at a higher issue latency.  0 (default) =
+                            never; 1e-300 = always.  Same arithmetic either way. */
 } asaga_options;
 
 typedef struct {
@@ -98,6 +104,7 @@ typedef struct {
   int64_t max_row;        /* longest row */
   int grid, block;        /* launch shape of the update kernel */
   double last_run_ms;     /* device time of the last blocking asaga_run (CUDA events) */
+  double bulk_scatter_min_freq;
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

@@ -53,6 +53,7 @@ struct asaga_ctx {
   double* y = nullptr;
   double2* xa = nullptr;   // {x_v, abar_v} pairs at xa[v * S]
   int S = 1;               // pair stride
+  double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
   double* D = nullptr;     // reweighting n / n_v
   double* dv = nullptr;    // D_{c_k} per stored entry
   double* alpha = nullptr;  // folded alpha~ = b alpha
@@ -149,28 +150,46 @@ int grid_for(const asaga_ctx* ctx, int64_t work, int block) {
 
 using UpdFn = void (*)(UpdateParams);
 
+template <int G, int NR, bool DET>
+UpdFn pick_mode(int mode) {
+  switch (mode) {
+    case 0: return asaga_update_kernel<G, NR, DET, 0>;
+    case 2: return asaga_update_kernel<G, NR, DET, 2>;
+    default: return asaga_update_kernel<G, NR, DET, 1>;
+  }
+}
+
 template <int G, int NR>
-UpdFn pick_upd(bool det, bool atomic) {
-  if (det) return atomic ? asaga_update_kernel<G, NR, true, true> : asaga_update_kernel<G, NR, true, false>;
-  return atomic ? asaga_update_kernel<G, NR, false, true> : asaga_update_kernel<G, NR, false, false>;
+UpdFn pick_upd(bool det, int mode) {
+  return det ? pick_mode<G, NR, true>(mode) : pick_mode<G, NR, false>(mode);
 }
 
 template <int G>
-UpdFn pick_upd_nr(int nr, bool det, bool atomic) {
+UpdFn pick_upd_nr(int nr, bool det, int mode) {
   switch (nr) {
-    case 1: return pick_upd<G, 1>(det, atomic);
-    case 2: return pick_upd<G, 2>(det, atomic);
-    case 4: return pick_upd<G, 4>(det, atomic);
-    default: return pick_upd<G, 8>(det, atomic);
+    case 1: return pick_upd<G, 1>(det, mode);
+    case 2: return pick_upd<G, 2>(det, mode);
+    case 4: return pick_upd<G, 4>(det, mode);
+    default: return pick_upd<G, 8>(det, mode);
   }
 }
 
-UpdFn update_fn(int lanes, int nr, bool det, bool atomic) {
+// scatter mode: 0 non-atomic ablation, 1 LSU REDs, 2 TMA bulk pair reductions
+int scatter_mode(const asaga_ctx* ctx);
+
+UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
+  const bool det = ctx->deterministic != 0;
+  const int mode = scatter_mode(ctx);
   switch (lanes) {
-    case 8: return pick_upd_nr<8>(nr, det, atomic);
-    case 16: return pick_upd_nr<16>(nr, det, atomic);
-    default: return pick_upd_nr<32>(nr, det, atomic);
+    case 8: return pick_upd_nr<8>(nr, det, mode);
+    case 16: return pick_upd_nr<16>(nr, det, mode);
+    default: return pick_upd_nr<32>(nr, det, mode);
   }
+}
+
+int scatter_mode(const asaga_ctx* ctx) {
+  if (!ctx->atomic_mode) return 0;
+  return ctx->bulk_dmax > 0.0 ? 2 : 1;
 }
 
 // Spread `workers` groups over all SMs: the smallest power-of-two block (>= one
@@ -199,14 +218,17 @@ asaga_status configure_update(asaga_ctx* ctx) {
   ctx->lanes = lanes;
   ctx->nr = nr;
   ctx->overflow = (int)std::max<int64_t>(0, ctx->max_row - (int64_t)nr * lanes);
+  ctx->overflow = (ctx->overflow + 1) & ~1;  // keep every group's smem block 16-byte aligned
   const int groups_per_block = kBlock / lanes;
   // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
   // (GroupSmem in asaga_kernels.cuh)
-  const size_t group_bytes = 2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
+  // (GroupSmem: bulk-scatter source buffer + 2 row stages + overflow q slots)
+  const size_t group_bytes = (size_t)nr * lanes * 2 * sizeof(double) +
+                             2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
                              (size_t)ctx->overflow * sizeof(double);
   ctx->group_bytes = group_bytes;
   ctx->smem = (size_t)groups_per_block * group_bytes;
-  UpdFn fn = update_fn(lanes, nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
+  UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 227 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
                 (long long)ctx->max_row);
@@ -236,7 +258,9 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   // 1 KiB block so hot features spread over L2 slices (2.2x at 1024 in flight,
   // profiles/r01_update_kernel.md); larger d keeps pairs dense (S = 8 measured no gain on c3).
   ctx->S = d <= 4096 ? 64 : 1;
+#ifdef ASAGA_TIMING
   if (const char* e = getenv("ASAGA_PAIR_STRIDE")) ctx->S = std::max(1, atoi(e));  // experiments
+#endif
   TRY(dalloc(ctx, &ctx->xa, (size_t)d * ctx->S));
   TRY(dalloc(ctx, &ctx->D, d));
   TRY(dalloc(ctx, &ctx->dv, nnz));
@@ -373,6 +397,13 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   ctx->record = o.record_samples ? 1 : 0;
   ctx->concurrency_opt = o.concurrency;
   ctx->lanes_opt = o.lanes_per_sample;
+  if (!(o.bulk_scatter_min_freq >= 0.0) || o.bulk_scatter_min_freq > 1.0) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG, "bulk_scatter_min_freq must be in [0, 1] (got %g)",
+                o.bulk_scatter_min_freq);
+  }
+  // p_v = n_v / n >= f  <=>  D_v = n / n_v <= 1 / f
+  ctx->bulk_dmax = o.bulk_scatter_min_freq > 0.0 ? 1.0 / o.bulk_scatter_min_freq : 0.0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
   if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
@@ -536,11 +567,12 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.T = n_updates;
   p.workers = ctx->workers;
   p.overflow = ctx->overflow;
+  p.bulk_dmax = ctx->bulk_dmax;
   p.debug_mode = 0;
 #ifdef ASAGA_TIMING
   if (const char* m = getenv("ASAGA_DEBUG_MODE")) p.debug_mode = atoi(m);
 #endif
-  UpdFn fn = update_fn(ctx->lanes, ctx->nr, ctx->deterministic != 0, ctx->atomic_mode != 0);
+  UpdFn fn = update_fn(ctx, ctx->lanes, ctx->nr);
   // Fewer updates than workers: launch only what is needed.  The stride stays W,
   // so the t -> worker map does not depend on the launch.
   int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
@@ -569,6 +601,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->atomic_mode = 1;
   opt->record_samples = 0;
   opt->stream = nullptr;
+  opt->bulk_scatter_min_freq = 0.0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -810,6 +843,7 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->grid = ctx->grid;
   out->block = ctx->block;
   out->last_run_ms = ctx->last_ms;
+  out->bulk_scatter_min_freq = ctx->bulk_dmax > 0.0 ? 1.0 / ctx->bulk_dmax : 0.0;
   return ASAGA_OK;
 }
 

@@ -284,6 +284,8 @@ struct UpdateParams {
   uint64_t seed, t0, T;
   int64_t workers;
   int overflow;         // shared-memory q slots per group (>= max_row - NR*G, or 0)
+  double bulk_dmax;     // MODE 2: entries with D_c <= bulk_dmax (popular features,
+                        // p_c >= 1/bulk_dmax) use the TMA bulk pair reduction, others REDs
   int debug_mode;       // profiling build only: bit0 skip the scatter, bit1 skip exp/div
 };
 
@@ -301,23 +303,42 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// Shared memory per group: 2 stages x P = NR*G row entries (fp64 value, fp64 D,
-// int32 index), then `overflow` fp64 q slots for rows longer than P.
+// Shared memory per group: a P-entry {dx, dabar} source buffer for the TMA bulk
+// scatter (16-B aligned, first), 2 stages x P = NR*G row entries (fp64 value,
+// fp64 D, int32 index), then `overflow` fp64 q slots for rows longer than P.
 template <int G, int NR>
 struct GroupSmem {
   static constexpr int P = NR * G;
+  static constexpr size_t delta_bytes = (size_t)P * 2 * sizeof(double);
   static constexpr size_t stage_bytes = (size_t)P * (2 * sizeof(double) + sizeof(int32_t));
   static __host__ __device__ size_t bytes(int overflow) {
-    return 2 * stage_bytes + (size_t)overflow * sizeof(double);
+    return delta_bytes + 2 * stage_bytes + (size_t)overflow * sizeof(double);
   }
 };
+
+// TMA bulk reduction of one {x, abar} pair: a single 16-byte .add.f64 performed at
+// L2 by the async proxy (UBLKRED) -- one L2 operation instead of two REDs on the
+// feature's line, and no LSU wavefronts (profiles/r01_update_kernel.md).
+__device__ __forceinline__ void bulk_red_pair(double2* gdst, const double2* ssrc) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], 16;" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(ssrc)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 template <int G, int NR>
 __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, const int32_t* cols,
                                                const double* vals, const double* dv, int64_t lo,
                                                int64_t hi, int g) {
   constexpr int P = NR * G;
-  double* sv = reinterpret_cast<double*>(base + stage * GroupSmem<G, NR>::stage_bytes);
+  double* sv = reinterpret_cast<double*>(base + GroupSmem<G, NR>::delta_bytes +
+                                         stage * GroupSmem<G, NR>::stage_bytes);
   double* sd = sv + P;
   int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
 #pragma unroll
@@ -350,8 +371,13 @@ __device__ unsigned long long g_phase_cycles[8];
   } while (0)
 #endif
 
-template <int G, int NR, bool DET, bool ATOMIC>
+// MODE: 0 = plain load + store (non-atomic ablation), 1 = red.global.add.f64 per
+// element (LSU), 2 = hybrid: one TMA bulk 16-byte reduction per {x, abar} pair of
+// a popular feature (D_c <= bulk_dmax: its L2 line is the bottleneck), REDs for the
+// rest (the bulk op is issued lane by lane, ~64 cycles each).
+template <int G, int NR, bool DET, int MODE>
 __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
+  constexpr bool ATOMIC = MODE != 0;
 #ifdef ASAGA_TIMING
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
@@ -365,7 +391,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
   if (w >= p.workers) return;
   unsigned char* gbase = smem_raw + (size_t)(threadIdx.x / G) * GroupSmem<G, NR>::bytes(p.overflow);
-  double* qs = reinterpret_cast<double*>(gbase + 2 * GroupSmem<G, NR>::stage_bytes);
+  double2* dbuf = reinterpret_cast<double2*>(gbase);
+  double* qs = reinterpret_cast<double*>(gbase + GroupSmem<G, NR>::delta_bytes +
+                                         2 * GroupSmem<G, NR>::stage_bytes);
 
   const uint64_t tend = p.t0 + p.T;
   uint64_t t = p.t0 + (uint64_t)w;
@@ -388,7 +416,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     // ---- pass 1: row entries (shared memory), gathers, dot product
     cp_async_wait_all();
     TMARK(0);
-    const double* sv = reinterpret_cast<const double*>(gbase + stage * GroupSmem<G, NR>::stage_bytes);
+    const double* sv = reinterpret_cast<const double*>(gbase + GroupSmem<G, NR>::delta_bytes +
+                                                       stage * GroupSmem<G, NR>::stage_bytes);
     const double* sd = sv + P;
     const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
     // gathers of x^, abar^ and D for every resident chunk are issued before any use
@@ -442,6 +471,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #endif
     // ---- pass 2: unlocked scatter (Property 3: atomic adds, no locks); row entries
     //      are re-read from the stage buffer, which is only overwritten next iteration
+    if (MODE == 2) bulk_wait_read();  // the previous sample's bulk ops have read dbuf
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       if (lo + j * G >= hi) break;  // group-uniform
@@ -451,7 +481,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         const double a = sv[j * G + g];
         const double u = fma(da, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
-        if (ATOMIC) {
+        if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
+          dbuf[j * G + g] = make_double2(ngam * u, da * a * p.inv_n);
+        } else if (MODE >= 1) {
           red_add(xv, ngam * u);
           red_add(xv + 1, da * a * p.inv_n);
         } else {
@@ -459,6 +491,17 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
           st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
         }
       }
+    }
+    if (MODE == 2) {
+      fence_proxy_async_smem();
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (lo + j * G >= hi) break;
+        const int64_t k = lo + j * G + g;
+        if (k < hi && sd[j * G + g] <= p.bulk_dmax)
+          bulk_red_pair(p.xa + (int64_t)sc[j * G + g] * p.S, dbuf + j * G + g);
+      }
+      bulk_commit();
     }
     for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
@@ -483,6 +526,10 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       if (p.visits) atomicAdd(p.visits + i, 1);
     }
     if (DET) {
+      if (MODE == 2) {
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       __threadfence();
       __syncwarp(gmask);
     }
@@ -498,6 +545,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     stage ^= 1;
   }
   cp_async_wait_all();
+  if (MODE == 2) bulk_wait_all();
 #ifdef ASAGA_TIMING
   if (g == 0)
     for (int k = 0; k < 6; ++k) atomicAdd(&g_phase_cycles[k], ph[k]);

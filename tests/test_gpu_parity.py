@@ -75,10 +75,11 @@ def test_sampler_bitexact(n, seed, t0):
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
-def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9):
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0):
     m = asaga_mod()
     g = gamma_of(prob)
-    a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes)
+    a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
+                             bulk_scatter_min_freq=bulk)
     st = oracle.State(prob.n, prob.d)
     D = oracle.reweight(prob.n, oracle.column_counts(prob))
     done = 0
@@ -110,6 +111,14 @@ def test_deterministic_c1_twenty_epochs():
 def test_deterministic_lane_groupings(lanes):
     p = datagen.make("c1")
     _det_compare(p, 3000, [1, 2, 37, 1000, 3000], lanes=lanes)
+
+
+@gpu
+@pytest.mark.parametrize("bulk", [1e-300, 0.05])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_deterministic_bulk_scatter(name, bulk):
+    """The TMA bulk pair reduction (all features, or the popular ones) is the same arithmetic."""
+    _det_compare(SUBSETS[name](), 20_000, [1, 5_000, 20_000], bulk=bulk)
 
 
 @gpu
@@ -258,8 +267,9 @@ def test_async_c1_epochs_within_1p5x_oracle(conc):
 
 
 @gpu
+@pytest.mark.parametrize("bulk", [0.0, 0.5, 1e-300])
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
-def test_async_sample_stream_and_quiescent_identity(name):
+def test_async_sample_stream_and_quiescent_identity(name, bulk):
     """Every t is processed exactly once (visit histogram == oracle's stream histogram,
     bit-exact) and, once quiescent, abar == (1/n) sum alpha_i a_i (no lost update)."""
     import scipy.sparse
@@ -267,7 +277,7 @@ def test_async_sample_stream_and_quiescent_identity(name):
     m = asaga_mod()
     p = SUBSETS[name]()
     T = 5 * p.n + 12345
-    a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True)
+    a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True, bulk_scatter_min_freq=bulk)
     a.run(T, SEED)
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)

@@ -108,6 +108,34 @@ __global__ void k_pair_hot(double* tab, uint32_t k, int iters) {
   }
 }
 
+// TMA bulk reduction: one cp.reduce.async.bulk .add.f64 of 16 bytes per pair
+// (both x and abar) from shared memory -- UBLKRED, issued lane by lane.
+// hot: lane 0 of each warp on k pairs 1 KiB apart (with the pair load);
+// random: every lane on a random pair of a d-pair table.
+__global__ void k_bulk_pair(double* tab, uint32_t k, uint32_t d, int iters, int hot) {
+  __shared__ __align__(16) double s[2 * 256];
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (hot && (threadIdx.x & 31) != 0) return;
+  s[2 * threadIdx.x] = 1.0;
+  s[2 * threadIdx.x + 1] = 1.0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s + 2 * threadIdx.x);
+  double acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    double* a = hot ? tab + (size_t)(((tid >> 5) + it) % k) * 128
+                    : tab + (size_t)(hash32(tid * 977u + it * 0x9E3779B9u) % d) * 2;
+    if (hot) {
+      double v0, v1;
+      asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v0), "=d"(v1) : "l"(a));
+      acc += v0 + v1;
+    }
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], 16;" ::"l"(a),
+                 "r"(sa + (acc == 12345.0 ? 16u : 0u)) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void k_red_list(double* tab, const uint32_t* __restrict__ list, uint64_t m, uint32_t stride) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x)
     asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)__ldg(list + j) * stride), "d"(1.0) : "memory");
@@ -292,6 +320,22 @@ int main(int argc, char** argv) {
       CK(cudaFree(tab));
     }
     js += "}";
+  }
+  // M4c TMA bulk 16-byte reductions (x and abar in one op)
+  {
+    double* tab;
+    const uint32_t d = 47236;
+    CK(cudaMalloc(&tab, (size_t)d * 128 * 8));
+    CK(cudaMemset(tab, 0, (size_t)d * 128 * 8));
+    const int blocks = sms * 8, threads = 256, iters = 32;
+    float ms_hot = best_ms([&] { k_bulk_pair<<<blocks, threads>>>(tab, 10, d, iters, 1); });
+    const double g_hot = (double)blocks * (threads / 32) * iters;
+    float ms_rnd = best_ms([&] { k_bulk_pair<<<blocks, threads>>>(tab, 10, d, iters, 0); });
+    const double g_rnd = (double)blocks * threads * iters;
+    snprintf(buf, sizeof buf, ", \"bulk_pair\": {\"hot_k10_updates_per_s_per_pair\": %.4g, \"random_pairs_per_s\": %.4g}",
+             g_hot / ms_hot * 1e3 / 10, g_rnd / ms_rnd * 1e3);
+    js += buf;
+    CK(cudaFree(tab));
   }
   // M5 Zipf RED pattern
   {

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--gscale", type=float, default=0.25)
     ap.add_argument("--atomic", type=int, default=1)
     ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     args = ap.parse_args()
     import importlib.util
 
@@ -39,7 +40,8 @@ def main():
     dev = torch.device("cuda", 0)
     t = lambda a: torch.from_numpy(a).to(dev)
     a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0,
-              atomic=bool(args.atomic), lanes_per_sample=args.lanes)
+              atomic=bool(args.atomic), lanes_per_sample=args.lanes,
+              bulk_scatter_min_freq=args.bulk)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     buf = (ctypes.c_ulonglong * 6)()
     names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail"]

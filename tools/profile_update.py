@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--conc", type=int, default=0)
     ap.add_argument("--gscale", type=float, default=0.25)
     ap.add_argument("--updates", type=int, default=0, help="default: one epoch")
+    ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -25,7 +26,8 @@ def main():
     p = datagen.make(args.cfg)
     dev = torch.device("cuda", 0)
     t = lambda a: torch.from_numpy(a).to(dev)
-    a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc)
+    a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc,
+              bulk_scatter_min_freq=args.bulk)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     T = args.updates or p.n
     a.run(T, datagen.SAMPLE_SEED)  # warm-up launch
