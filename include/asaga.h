@@ -90,6 +90,11 @@ typedef struct {
                             operation on the feature's line instead of two (the hot line is
                             the throughput bound), at a higher issue latency.  0 (default) =
                             never; 1e-300 = always.  Same arithmetic either way. */
+  int measure_overlap;   /* k > 0: estimate the overlap tau (App. D): a
+                            sparse global counter is advanced by 100 per 100 updates of each
+                            worker, and every k-th sample of a worker records the counter's
+                            advance between its read and its write; mean / max in
+                            asaga_stats.  0 (default) = off (no counter traffic). */
 } asaga_options;
 
 typedef struct {
@@ -105,6 +110,9 @@ typedef struct {
   int grid, block;        /* launch shape of the update kernel */
   double last_run_ms;     /* device time of the last blocking asaga_run (CUDA events) */
   double bulk_scatter_min_freq;
+  double overlap_mean;    /* measure_overlap: mean per-sample overlap estimate since ingest */
+  int64_t overlap_max;    /* ... and the largest one */
+  int64_t overlap_samples;
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

@@ -40,7 +40,8 @@ class Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("deterministic", ctypes.c_int),
                 ("concurrency", ctypes.c_int64), ("lanes_per_sample", ctypes.c_int),
                 ("atomic_mode", ctypes.c_int), ("record_samples", ctypes.c_int),
-                ("stream", ctypes.c_void_p), ("bulk_scatter_min_freq", ctypes.c_double)]
+                ("stream", ctypes.c_void_p), ("bulk_scatter_min_freq", ctypes.c_double),
+                ("measure_overlap", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -50,7 +51,8 @@ class Stats(ctypes.Structure):
                 ("concurrency", ctypes.c_int64), ("lanes_per_sample", ctypes.c_int),
                 ("deterministic", ctypes.c_int), ("max_row", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("block", ctypes.c_int), ("last_run_ms", ctypes.c_double),
-                ("bulk_scatter_min_freq", ctypes.c_double)]
+                ("bulk_scatter_min_freq", ctypes.c_double), ("overlap_mean", ctypes.c_double),
+                ("overlap_max", ctypes.c_int64), ("overlap_samples", ctypes.c_int64)]
 
 
 ABI_FUNCTIONS = {
@@ -153,7 +155,7 @@ class Asaga:
     def __init__(self, indptr, indices, data, y, d: int, lam: float, gamma: float, *,
                  deterministic: bool = False, concurrency: int = 0, lanes_per_sample: int = 0,
                  atomic: bool = True, record_samples: bool = False, device: int = 0,
-                 stream=None, bulk_scatter_min_freq: float = 0.0):
+                 stream=None, bulk_scatter_min_freq: float = 0.0, measure_overlap: int = 0):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -172,6 +174,7 @@ class Asaga:
         opt.record_samples = int(bool(record_samples))
         opt.stream = stream
         opt.bulk_scatter_min_freq = float(bulk_scatter_min_freq)
+        opt.measure_overlap = int(measure_overlap)
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

@@ -59,6 +59,8 @@ struct asaga_ctx {
   double* alpha = nullptr;  // folded alpha~ = b alpha
   int32_t* counts = nullptr;
   int32_t* visits = nullptr;
+  unsigned long long* ov = nullptr;  // overlap instrumentation (4 counters)
+  int ov_every = 0;
   // scratch
   double* sig = nullptr;
   double* block_loss = nullptr;
@@ -275,6 +277,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->flag, 4));
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 2));  // err rows, max ||a||^2, max row
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
+  if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
   return ASAGA_OK;
 }
 
@@ -287,6 +290,7 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
+  if (ctx->ov) CK(ctx, cudaMemsetAsync(ctx->ov, 0, 4 * sizeof(unsigned long long), ctx->stream));
   CK(ctx, cudaMemsetAsync(ctx->counts, 0, sizeof(int32_t) * d, ctx->stream));
   CK(ctx, cudaMemsetAsync(ctx->alpha, 0, sizeof(double) * n, ctx->stream));
   CK(ctx, cudaMemsetAsync(scratch, 0xff, sizeof(unsigned long long) * ERR_COUNT, ctx->stream));
@@ -395,6 +399,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   ctx->deterministic = o.deterministic ? 1 : 0;
   ctx->atomic_mode = o.atomic_mode ? 1 : 0;
   ctx->record = o.record_samples ? 1 : 0;
+  ctx->ov_every = o.measure_overlap > 0 ? o.measure_overlap : 0;
   ctx->concurrency_opt = o.concurrency;
   ctx->lanes_opt = o.lanes_per_sample;
   if (!(o.bulk_scatter_min_freq >= 0.0) || o.bulk_scatter_min_freq > 1.0) {
@@ -558,6 +563,8 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.S = ctx->S;
   p.alpha = ctx->alpha;
   p.visits = ctx->visits;
+  p.ov = ctx->ov;
+  p.ov_every = ctx->ov_every > 0 ? ctx->ov_every : 1;
   p.n = (uint64_t)ctx->n;
   p.gamma = ctx->gamma;
   p.lambda_ = ctx->lambda;
@@ -600,6 +607,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->lanes_per_sample = 0;
   opt->atomic_mode = 1;
   opt->record_samples = 0;
+  opt->measure_overlap = 0;
   opt->stream = nullptr;
   opt->bulk_scatter_min_freq = 0.0;
 }
@@ -844,6 +852,17 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->block = ctx->block;
   out->last_run_ms = ctx->last_ms;
   out->bulk_scatter_min_freq = ctx->bulk_dmax > 0.0 ? 1.0 / ctx->bulk_dmax : 0.0;
+  out->overlap_mean = 0.0;
+  out->overlap_max = 0;
+  out->overlap_samples = 0;
+  if (ctx->ov) {
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (cudaMemcpy(h, ctx->ov, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess && h[2] > 0) {
+      out->overlap_mean = (double)h[1] / (double)h[2];
+      out->overlap_max = (int64_t)h[3];
+      out->overlap_samples = (int64_t)h[2];
+    }
+  }
   return ASAGA_OK;
 }
 

@@ -279,6 +279,10 @@ struct UpdateParams {
   int S;                // pair stride
   double* alpha;        // folded alpha~
   int32_t* visits;      // NULL unless record_samples
+  unsigned long long* ov;  // NULL, or overlap instrumentation (NEXT-1, App. D):
+                           // [0] sparse global progress counter (+100 per 100 local samples),
+                           // [1] sum and [2] count of per-sample overlap estimates, [3] max
+  int ov_every;            // measure every ov_every-th local sample
   uint64_t n;
   double gamma, lambda_, inv_n;
   uint64_t seed, t0, T;
@@ -412,7 +416,13 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   }
   if (t + 2 * W < tend) in2 = sample_row(p.seed, t + 2 * W, p.n);
 
+  unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
+  int ov_local = 0, ov_iter = 0;
   while (true) {
+    // overlap estimate (App. D): progress counter at the read and after the write
+    const bool ov_meas = p.ov != nullptr && (ov_iter++ % p.ov_every) == 0;
+    unsigned long long ov_c0 = 0;
+    if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
     // ---- pass 1: row entries (shared memory), gathers, dot product
     cp_async_wait_all();
     TMARK(0);
@@ -524,6 +534,20 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       if (ATOMIC) red_add(p.alpha + i, da);
       else st_cg(p.alpha + i, ai + da);
       if (p.visits) atomicAdd(p.visits + i, 1);
+      if (p.ov != nullptr) {
+        if (++ov_local == 100) {  // sparse counter: one +100 per 100 local updates
+          atomicAdd(p.ov, 100ull);
+          ov_local = 0;
+        }
+        if (ov_meas) {
+          unsigned long long c1;
+          asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c1) : "l"(p.ov));
+          const unsigned long long o = c1 - ov_c0;
+          ov_sum += o;
+          ov_cnt += 1;
+          ov_max = max(ov_max, o);
+        }
+      }
     }
     if (DET) {
       if (MODE == 2) {
@@ -546,6 +570,11 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   }
   cp_async_wait_all();
   if (MODE == 2) bulk_wait_all();
+  if (p.ov != nullptr && g == 0 && ov_cnt > 0) {
+    atomicAdd(p.ov + 1, ov_sum);
+    atomicAdd(p.ov + 2, ov_cnt);
+    atomicMax(p.ov + 3, ov_max);
+  }
 #ifdef ASAGA_TIMING
   if (g == 0)
     for (int k = 0; k < 6; ++k) atomicAdd(&g_phase_cycles[k], ph[k]);

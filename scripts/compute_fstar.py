@@ -21,7 +21,7 @@ import datagen  # noqa: E402
 import oracle  # noqa: E402
 
 
-def main(cfgs):
+def main(cfgs, bound_target=1e-12, max_polish=200):
     for cfg in cfgs:
         p = datagen.make(cfg)
         L = oracle.lipschitz(p, p.lam)
@@ -37,17 +37,20 @@ def main(cfgs):
             oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, step, st, D)
             trace.append(oracle.objective(p, p.y, p.lam, st.x))
             epochs += 1
+            if epochs % 10 == 0:
+                print(f"  epoch {epochs / 10:.1f}: f={trace[-1]:.15f}", flush=True)
             if len(trace) > 40 and abs(trace[-1] - trace[-11]) < 1e-15 * abs(trace[-1]):
                 break
         # polish: keep running until the certificate is below 1e-9 (or stops improving)
         best = None
-        for _ in range(200):
+        for _ in range(max_polish):
             g = oracle.full_grad(p, p.y, p.lam, st.x)
             gn = float(np.linalg.norm(g))
             f = oracle.objective(p, p.y, p.lam, st.x)
             if best is None or gn < best[1]:
                 best = (f, gn)
-            if gn ** 2 / (2 * p.lam) <= 1e-12:
+            print(f"  polish: f={f:.15f} |grad|={gn:.3e} bound={gn ** 2 / (2 * p.lam):.3e}", flush=True)
+            if gn ** 2 / (2 * p.lam) <= bound_target:
                 break
             oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, 5 * p.n, st, D)
         f_star, gnorm = best
@@ -71,4 +74,7 @@ def main(cfgs):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c2", "c3"])
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    big = "--big" in sys.argv  # c4: certificate target 1e-10, at most 12 polish rounds of 5 epochs
+    main(args or ["c1", "c2", "c3"], bound_target=1e-10 if big else 1e-12,
+         max_polish=12 if big else 200)
