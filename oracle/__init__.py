@@ -17,6 +17,8 @@ Functions and the passages they follow:
   objective / full_grad         Section 4.1
   sparse_saga                   Eq. 3 + Section 4.2, Alg. 2 order
   delayed_saga                  Assumption 1 at its bound; NEXT-1 tool
+  hogwild / svrg_*              Section 4.3 comparison methods, SPEC S:230-237,
+                                S:306-307, regulariser projected as in Section 4.2 (R21)
 All are pinned in tests/test_oracle_pins.py; none is "parity unpinned".
 """
 from __future__ import annotations
@@ -78,6 +80,12 @@ def _load():
                                                _F64P]),
             "oracle_delayed_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                            u64, u64, u64, i64, _F64P, _F64P, _F64P]),
+            "oracle_hogwild": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
+                                      u64, u64, u64, _F64P]),
+            "oracle_svrg_snapshot": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, _F64P,
+                                            _F64P]),
+            "oracle_svrg_inner": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
+                                         u64, u64, u64, _F64P, _F64P, _F64P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -246,3 +254,38 @@ def delayed_saga(A, y, lam, gamma, seed, T: int, tau: int, state: State | None =
                                 _p(state.alpha_bar, _F64P))
     state.t += T
     return state
+
+
+def hogwild(A, y, lam, gamma, seed, t0: int, T: int, x: np.ndarray, D=None) -> np.ndarray:
+    """HOGWILD's serial form (sparse SGD), updates t0..t0+T-1, x in place."""
+    n, d, indptr, indices, data = _csr(A)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if D is None:
+        D = reweight(n, column_counts(A))
+    _load().oracle_hogwild(n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P),
+                           _p(y, _F64P), _p(D, _F64P), lam, gamma, seed, t0, T, _p(x, _F64P))
+    return x
+
+
+def svrg_snapshot(A, y, xref: np.ndarray):
+    """KROMAGNON's synchronised phase: (s_i = sigma_i(x~), mu = (1/n) sum s_i a_i)."""
+    n, d, indptr, indices, data = _csr(A)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    xref = np.ascontiguousarray(xref, dtype=np.float64)
+    s = np.empty(n)
+    mu = np.empty(d)
+    _load().oracle_svrg_snapshot(n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P),
+                                 _p(y, _F64P), _p(xref, _F64P), _p(s, _F64P), _p(mu, _F64P))
+    return s, mu
+
+
+def svrg_inner(A, y, lam, gamma, seed, t0: int, T: int, s, mu, x: np.ndarray, D=None):
+    """KROMAGNON inner steps t0..t0+T-1 against a snapshot (s, mu); x in place."""
+    n, d, indptr, indices, data = _csr(A)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if D is None:
+        D = reweight(n, column_counts(A))
+    _load().oracle_svrg_inner(n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P),
+                              _p(y, _F64P), _p(D, _F64P), lam, gamma, seed, t0, T,
+                              _p(s, _F64P), _p(mu, _F64P), _p(x, _F64P))
+    return x

@@ -279,3 +279,71 @@ void oracle_delayed_saga(int64_t n, int64_t d, const int64_t* indptr,
   for (int64_t s = 0; s < slots; ++s) free(ring[s].u);
   free(ring);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Comparison methods of Section 4.3, NEXT-2.  Both follow SPEC's
+ * serial forms with the D_i-projected regulariser of
+ * Section 4.2 applied uniformly (reading R21).
+ *
+ * HOGWILD (Niu et al.): sparse SGD with constant step,
+ *   x_v <- x_v - gamma (sigma_i(x) a_iv + lambda D_v x_v),  v in S_i.          */
+void oracle_hogwild(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                    const double* data, const double* y, const double* D, double lambda,
+                    double gamma, uint64_t seed, uint64_t t0, uint64_t T, double* x) {
+  (void)d;
+  int64_t maxrow = 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] - indptr[i] > maxrow) maxrow = indptr[i + 1] - indptr[i];
+  double* u = (double*)malloc(sizeof(double) * (size_t)maxrow);
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double s = oracle_sigma(y[i], z);
+    for (int64_t k = lo; k < hi; ++k) u[k - lo] = s * data[k] + lambda * D[indices[k]] * x[indices[k]];
+    for (int64_t k = lo; k < hi; ++k) x[indices[k]] = x[indices[k]] - gamma * u[k - lo];
+  }
+  free(u);
+}
+
+/* KROMAGNON (sparse SVRG of Mania et al.): the synchronised phase
+ * caches s_i = sigma_i(x~) for every i and mu = (1/n) sum_i s_i a_i (the data part
+ * of grad f(x~)); the inner steps are
+ *   x_v <- x_v - gamma ((sigma_i(x) - s_i) a_iv + D_v mu_v + lambda D_v x_v).     */
+void oracle_svrg_snapshot(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                          const double* data, const double* y, const double* xref, double* s,
+                          double* mu) {
+  for (int64_t v = 0; v < d; ++v) mu[v] = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double z = 0.0;
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) z += data[k] * xref[indices[k]];
+    s[i] = oracle_sigma(y[i], z);
+    for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) mu[indices[k]] += s[i] * data[k];
+  }
+  for (int64_t v = 0; v < d; ++v) mu[v] = mu[v] / (double)n;
+}
+
+void oracle_svrg_inner(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                       const double* data, const double* y, const double* D, double lambda,
+                       double gamma, uint64_t seed, uint64_t t0, uint64_t T, const double* s,
+                       const double* mu, double* x) {
+  (void)d;
+  int64_t maxrow = 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] - indptr[i] > maxrow) maxrow = indptr[i + 1] - indptr[i];
+  double* u = (double*)malloc(sizeof(double) * (size_t)maxrow);
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double dsig = oracle_sigma(y[i], z) - s[i];
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      u[k - lo] = dsig * data[k] + D[v] * mu[v] + lambda * D[v] * x[v];
+    }
+    for (int64_t k = lo; k < hi; ++k) x[indices[k]] = x[indices[k]] - gamma * u[k - lo];
+  }
+  free(u);
+}

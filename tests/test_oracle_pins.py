@@ -426,3 +426,87 @@ def test_delayed_tau1_by_hand():
     st.x += pending[0]; st.alpha += pending[1]; st.alpha_bar += pending[2]
     assert np.allclose(got.x, st.x, rtol=1e-14, atol=1e-15)
     assert np.allclose(got.alpha, st.alpha, rtol=1e-14, atol=1e-15)
+
+
+# --------------------------------------------------------------------------- NEXT-2 comparison methods
+def test_svrg_first_inner_step_reference_identity():
+    """At x = x~ the data difference vanishes: the step is -gamma (D mu + lambda D x) on S_i."""
+    p = datagen.random_tiny(41, 30, 12, density=0.4)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+    x0 = np.random.default_rng(1).standard_normal(p.d)
+    s, mu = oracle.svrg_snapshot(p, p.y, x0)
+    x = oracle.svrg_inner(p, p.y, p.lam, 0.3, SEED, 0, 1, s, mu, x0.copy(), D)
+    i = oracle.sample_index(SEED, 0, p.n)
+    S = p.indices[p.indptr[i]:p.indptr[i + 1]]
+    want = x0.copy()
+    want[S] = x0[S] - 0.3 * (D[S] * mu[S] + p.lam * D[S] * x0[S])
+    assert np.allclose(x, want, rtol=1e-15, atol=1e-15)
+
+
+def test_svrg_snapshot_is_data_gradient():
+    p = datagen.random_tiny(42, 25, 9)
+    x0 = np.random.default_rng(2).standard_normal(p.d)
+    s, mu = oracle.svrg_snapshot(p, p.y, x0)
+    # mu + lambda x~ is grad f(x~) (pinned by finite differences, P6)
+    assert np.allclose(mu + p.lam * x0, oracle.full_grad(p, p.y, p.lam, x0), rtol=1e-13, atol=1e-15)
+    A = datagen.to_dense(p)
+    assert np.allclose(s, -p.y / (1 + np.exp(p.y * (A @ x0))), rtol=1e-14)
+
+
+def test_svrg_and_hogwild_are_saga_with_frozen_memory():
+    """Cross-check of three independently written oracle updates: SVRG's inner step equals
+    the Sparse SAGA step with the memory frozen at (s, mu); HOGWILD's with (0, 0)."""
+    p = datagen.random_tiny(43, 40, 15, density=0.3)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+    x0 = np.random.default_rng(3).standard_normal(p.d)
+    s, mu = oracle.svrg_snapshot(p, p.y, x0)
+    T = 300
+    xs = oracle.svrg_inner(p, p.y, p.lam, 0.2, SEED, 0, T, s, mu, x0.copy(), D)
+    xh = oracle.hogwild(p, p.y, p.lam, 0.2, SEED, 0, T, x0.copy(), D)
+    for frozen_a, frozen_ab, got in ((s, mu, xs), (np.zeros(p.n), np.zeros(p.d), xh)):
+        st = fresh(p)
+        st.x = x0.copy()
+        for i in oracle.sample_stream(SEED, 0, T, p.n):
+            st.alpha, st.alpha_bar = frozen_a.copy(), frozen_ab.copy()
+            oracle.saga_step(p, p.y, p.lam, 0.2, int(i), st, D)
+        assert np.allclose(got, st.x, rtol=1e-13, atol=1e-14)
+
+
+def test_svrg_hogwild_dense_reduce_to_textbook():
+    """On 100%-dense data (D = I): textbook SVRG inner steps and textbook SGD."""
+    p = datagen.random_tiny(44, 20, 6, dense=True)
+    A = datagen.to_dense(p)
+    b = p.y
+    x0 = np.random.default_rng(4).standard_normal(p.d)
+    s, mu = oracle.svrg_snapshot(p, p.y, x0)
+    T, g = 200, 0.25
+    x_svrg, x_sgd = x0.copy(), x0.copy()
+    for i in oracle.sample_stream(SEED, 0, T, p.n):
+        sig = -b[i] / (1 + np.exp(b[i] * (A[i] @ x_svrg)))
+        x_svrg = x_svrg - g * ((sig - s[i]) * A[i] + mu + p.lam * x_svrg)
+        sig2 = -b[i] / (1 + np.exp(b[i] * (A[i] @ x_sgd)))
+        x_sgd = x_sgd - g * (sig2 * A[i] + p.lam * x_sgd)
+    assert np.allclose(oracle.svrg_inner(p, p.y, p.lam, g, SEED, 0, T, s, mu, x0.copy()), x_svrg,
+                       rtol=1e-12, atol=1e-13)
+    assert np.allclose(oracle.hogwild(p, p.y, p.lam, g, SEED, 0, T, x0.copy()), x_sgd,
+                       rtol=1e-12, atol=1e-13)
+
+
+def test_hogwild_stalls_where_saga_converges():
+    """Constant-step SGD plateaus at a variance floor; SAGA/SVRG converge linearly
+    (the paper measures HOGWILD only to 1e-3)."""
+    p = datagen.make("c1")
+    L = oracle.lipschitz(p, p.lam)
+    g = 1 / (3 * L)
+    fstar = json.load(open(os.path.join(GOLDEN, "fstar_c1.json")))["f_star"]
+    x = oracle.hogwild(p, p.y, p.lam, g, SEED, 0, 50 * p.n, np.zeros(p.d))
+    saga = oracle.sparse_saga(p, p.y, p.lam, g, SEED, 50 * p.n)
+    xk = np.zeros(p.d)
+    t = 0
+    for _ in range(25):  # KROMAGNON: snapshot every 2 epochs
+        s, mu = oracle.svrg_snapshot(p, p.y, xk)
+        oracle.svrg_inner(p, p.y, p.lam, g, SEED, t, 2 * p.n, s, mu, xk)
+        t += 2 * p.n
+    assert oracle.objective(p, p.y, p.lam, x) - fstar > 1e-6
+    assert oracle.objective(p, p.y, p.lam, saga.x) - fstar < 1e-10
+    assert oracle.objective(p, p.y, p.lam, xk) - fstar < 1e-10
