@@ -45,6 +45,16 @@ extern "C" {
 
 typedef struct asaga_ctx asaga_ctx;
 
+/* The update rule run by asaga_run (NEXT-2: the paper's comparison methods, Section
+ * 4.3 PAPER.md:539-546, on the same kernel).  All three share the D_i-projected
+ * l2 term of Section 4.2 (reading R21). */
+typedef enum {
+  ASAGA_ALG_ASAGA = 0,     /* Algorithm 2 (default) */
+  ASAGA_ALG_KROMAGNON = 1, /* sparse SVRG: inner steps use the memory frozen at the last
+                              asaga_snapshot (alpha_i = sigma_i(x~), abar = data gradient) */
+  ASAGA_ALG_HOGWILD = 2    /* sparse SGD: memory frozen at zero */
+} asaga_algorithm;
+
 typedef enum {
   ASAGA_OK = 0,
   ASAGA_E_INVALID_ARG = 1, /* NULL pointer, lambda <= 0, gamma <= 0, n or d out of range */
@@ -113,6 +123,7 @@ typedef struct {
   double overlap_mean;    /* measure_overlap: mean per-sample overlap estimate since ingest */
   int64_t overlap_max;    /* ... and the largest one */
   int64_t overlap_samples;
+  int algorithm;          /* asaga_algorithm */
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */
@@ -194,6 +205,17 @@ ASAGA_API asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double
 /* Per-row visit counts (HOST int32[n]) since init or the last reset; needs
  * options.record_samples = 1, else ASAGA_E_STATE. reset != 0 zeroes them after the copy. */
 ASAGA_API asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset);
+
+/* Select the update rule (asaga_algorithm).  Switching to HOGWILD zeroes alpha and abar
+ * (its memory is identically 0); switching to KROMAGNON requires asaga_snapshot()
+ * before the next run (ASAGA_E_STATE otherwise).  x is kept. */
+ASAGA_API asaga_status asaga_set_algorithm(asaga_ctx* ctx, int algorithm);
+
+/* KROMAGNON's synchronised phase (Mania et al.): at the current x,
+ * alpha_i := sigma_i(x) for every i and abar := (1/n) sum_i alpha_i a_i (one row pass,
+ * one column pass), then the inner steps of asaga_run read this frozen memory.
+ * Blocking.  ASAGA_E_STATE unless the algorithm is KROMAGNON. */
+ASAGA_API asaga_status asaga_snapshot(asaga_ctx* ctx);
 
 /* Change the step size gamma (> 0) for subsequent runs. */
 ASAGA_API asaga_status asaga_set_gamma(asaga_ctx* ctx, double gamma);

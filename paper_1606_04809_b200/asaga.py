@@ -23,6 +23,9 @@ STATUS = {0: "ASAGA_OK", 1: "ASAGA_E_INVALID_ARG", 2: "ASAGA_E_BAD_CSR", 3: "ASA
           4: "ASAGA_E_CUDA", 5: "ASAGA_E_OOM", 6: "ASAGA_E_DIVERGED", 7: "ASAGA_E_STATE"}
 
 
+ALGORITHMS = {"asaga": 0, "kromagnon": 1, "hogwild": 2}
+
+
 class AsagaError(RuntimeError):
     def __init__(self, status: int, message: str):
         super().__init__(f"{STATUS.get(status, status)}: {message}")
@@ -52,7 +55,8 @@ class Stats(ctypes.Structure):
                 ("deterministic", ctypes.c_int), ("max_row", ctypes.c_int64),
                 ("grid", ctypes.c_int), ("block", ctypes.c_int), ("last_run_ms", ctypes.c_double),
                 ("bulk_scatter_min_freq", ctypes.c_double), ("overlap_mean", ctypes.c_double),
-                ("overlap_max", ctypes.c_int64), ("overlap_samples", ctypes.c_int64)]
+                ("overlap_max", ctypes.c_int64), ("overlap_samples", ctypes.c_int64),
+                ("algorithm", ctypes.c_int)]
 
 
 ABI_FUNCTIONS = {
@@ -81,6 +85,8 @@ ABI_FUNCTIONS = {
     "asaga_get_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "asaga_get_sample_counts": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
     "asaga_set_gamma": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
+    "asaga_set_algorithm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "asaga_snapshot": (ctypes.c_int, [ctypes.c_void_p]),
     "asaga_set_concurrency": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "asaga_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
     "asaga_sample_indices": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
@@ -274,6 +280,14 @@ class Asaga:
 
     def set_gamma(self, gamma: float) -> None:
         _check(_lib.asaga_set_gamma(self._h, float(gamma)), self._h)
+
+    def set_algorithm(self, name: str) -> None:
+        """'asaga' | 'kromagnon' | 'hogwild' (NEXT-2 comparison methods on the same kernel)."""
+        _check(_lib.asaga_set_algorithm(self._h, ALGORITHMS[name]), self._h)
+
+    def snapshot(self) -> None:
+        """KROMAGNON's synchronised phase at the current iterate."""
+        _check(_lib.asaga_snapshot(self._h), self._h)
 
     def set_concurrency(self, c: int) -> None:
         _check(_lib.asaga_set_concurrency(self._h, int(c)), self._h)

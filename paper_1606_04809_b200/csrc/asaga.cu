@@ -60,6 +60,8 @@ struct asaga_ctx {
   int32_t* counts = nullptr;
   int32_t* visits = nullptr;
   unsigned long long* ov = nullptr;  // overlap instrumentation (4 counters)
+  int algorithm = ASAGA_ALG_ASAGA;
+  bool snapshot_valid = false;       // KROMAGNON: alpha / abar hold a snapshot
   int ov_every = 0;
   // scratch
   double* sig = nullptr;
@@ -297,6 +299,7 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   CK(ctx, cudaMemsetAsync(scratch + ERR_COUNT, 0, sizeof(unsigned long long) * 2, ctx->stream));
   CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
   ctx->t = 0;
+  ctx->snapshot_valid = false;
   if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
     CK(ctx, cudaStreamSynchronize(ctx->stream));
     dfree(ctx, &ctx->csc_rows);
@@ -554,6 +557,8 @@ int current_xs(const asaga_ctx* ctx) { return 2 * ctx->S; }
 
 asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool timed) {
   if (n_updates == 0) return ASAGA_OK;
+  if (ctx->algorithm == ASAGA_ALG_KROMAGNON && !ctx->snapshot_valid)
+    return fail(ctx, ASAGA_E_STATE, "KROMAGNON needs asaga_snapshot() before asaga_run");
   UpdateParams p;
   p.rowptr = ctx->rowptr;
   p.cols = ctx->cols;
@@ -564,6 +569,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.alpha = ctx->alpha;
   p.visits = ctx->visits;
   p.ov = ctx->ov;
+  p.frozen = ctx->algorithm != ASAGA_ALG_ASAGA ? 1 : 0;
   p.ov_every = ctx->ov_every > 0 ? ctx->ov_every : 1;
   p.n = (uint64_t)ctx->n;
   p.gamma = ctx->gamma;
@@ -852,6 +858,7 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->block = ctx->block;
   out->last_run_ms = ctx->last_ms;
   out->bulk_scatter_min_freq = ctx->bulk_dmax > 0.0 ? 1.0 / ctx->bulk_dmax : 0.0;
+  out->algorithm = ctx->algorithm;
   out->overlap_mean = 0.0;
   out->overlap_max = 0;
   out->overlap_samples = 0;
@@ -897,6 +904,47 @@ const char* asaga_status_string(asaga_status s) {
     case ASAGA_E_STATE: return "ASAGA_E_STATE";
   }
   return "ASAGA_E_UNKNOWN";
+}
+
+asaga_status asaga_set_algorithm(asaga_ctx* ctx, int algorithm) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  if (algorithm != ASAGA_ALG_ASAGA && algorithm != ASAGA_ALG_KROMAGNON && algorithm != ASAGA_ALG_HOGWILD)
+    return fail(ctx, ASAGA_E_INVALID_ARG, "unknown algorithm %d", algorithm);
+  CK(ctx, cudaSetDevice(ctx->device));
+  ctx->algorithm = algorithm;
+  ctx->snapshot_valid = false;
+  if (algorithm == ASAGA_ALG_HOGWILD) {  // HOGWILD's memory is identically zero
+    CK(ctx, cudaMemsetAsync(ctx->alpha, 0, sizeof(double) * ctx->n, ctx->stream));
+    CK(ctx, cudaMemsetAsync(ctx->tmp_d2, 0, sizeof(double) * ctx->d, ctx->stream));
+    pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->xa, ctx->S, nullptr,
+                                                                              ctx->tmp_d2, ctx->d);
+    CK(ctx, cudaGetLastError());
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  return ASAGA_OK;
+}
+
+asaga_status asaga_snapshot(asaga_ctx* ctx) {
+  if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
+  if (ctx->algorithm != ASAGA_ALG_KROMAGNON)
+    return fail(ctx, ASAGA_E_STATE, "asaga_snapshot is the KROMAGNON synchronised phase");
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(ensure_csc(ctx));
+  cudaStream_t s = ctx->stream;
+  // alpha~_i := sigma~_i(x) (folded memory), abar := (1/n) sum_i alpha~_i a~_i
+  TRY(enqueue_objective(ctx, current_x(ctx), current_xs(ctx), ctx->scal, nullptr, true, s));
+  CK(ctx, cudaMemcpyAsync(ctx->alpha, ctx->sig, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, s));
+  const double lam = ctx->lambda;
+  ctx->lambda = 0.0;  // the data part only: colsum adds lambda x, so zero it for this pass
+  asaga_status st = enqueue_gradient(ctx, current_x(ctx), current_xs(ctx), ctx->tmp_d2, 1, s);
+  ctx->lambda = lam;
+  TRY(st);
+  pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->xa, ctx->S, nullptr, ctx->tmp_d2,
+                                                                  ctx->d);
+  CK(ctx, cudaGetLastError());
+  CK(ctx, cudaStreamSynchronize(s));
+  ctx->snapshot_valid = true;
+  return ASAGA_OK;
 }
 
 int asaga_abi_version(void) { return ASAGA_ABI_VERSION; }

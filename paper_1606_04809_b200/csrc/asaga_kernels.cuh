@@ -283,6 +283,9 @@ struct UpdateParams {
                            // [0] sparse global progress counter (+100 per 100 local samples),
                            // [1] sum and [2] count of per-sample overlap estimates, [3] max
   int ov_every;            // measure every ov_every-th local sample
+  int frozen;              // 1: the memory (alpha, abar) is read but never written --
+                           // KROMAGNON inner steps (alpha = sigma(x~), abar = mu) and
+                           // HOGWILD (alpha = abar = 0), NEXT-2
   uint64_t n;
   double gamma, lambda_, inv_n;
   uint64_t seed, t0, T;
@@ -492,13 +495,13 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         const double u = fma(da, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
-          dbuf[j * G + g] = make_double2(ngam * u, da * a * p.inv_n);
+          dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : da * a * p.inv_n);
         } else if (MODE >= 1) {
           red_add(xv, ngam * u);
-          red_add(xv + 1, da * a * p.inv_n);
+          if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
         } else {
           st_cg(xv, ld_cg(xv) + ngam * u);
-          st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
+          if (!p.frozen) st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
         }
       }
     }
@@ -520,10 +523,10 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       double* xv = &p.xa[(int64_t)c * p.S].x;
       if (ATOMIC) {
         red_add(xv, ngam * u);
-        red_add(xv + 1, da * a * p.inv_n);
+        if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
       } else {
         st_cg(xv, ld_cg(xv) + ngam * u);
-        st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
+        if (!p.frozen) st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
       }
     }
 #ifdef ASAGA_TIMING
@@ -531,8 +534,12 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #endif
     TMARK(3);
     if (g == 0) {
-      if (ATOMIC) red_add(p.alpha + i, da);
-      else st_cg(p.alpha + i, ai + da);
+      if (p.frozen) {
+      } else if (ATOMIC) {
+        red_add(p.alpha + i, da);
+      } else {
+        st_cg(p.alpha + i, ai + da);
+      }
       if (p.visits) atomicAdd(p.visits + i, 1);
       if (p.ov != nullptr) {
         if (++ov_local == 100) {  // sparse counter: one +100 per 100 local updates

@@ -417,3 +417,67 @@ def test_overlap_estimate_tracks_samples_in_flight():
     b = m.Asaga.from_problem(p, gamma_of(p))
     b.run(p.n, SEED)
     assert b.stats()["overlap_samples"] == 0
+
+
+# ---------------------------------------------------------------------- NEXT-2 comparison methods
+@gpu
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_hogwild_deterministic_matches_oracle(name):
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    a.set_algorithm("hogwild")
+    a.run(3 * p.n, SEED)
+    x, alpha, ab, _ = a.get_state()
+    ref = oracle.hogwild(p, p.y, p.lam, g, SEED, 0, 3 * p.n, np.zeros(p.d))
+    assert rel(x, ref) <= 1e-9
+    assert not alpha.any() and not ab.any()  # HOGWILD never writes its (zero) memory
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_kromagnon_deterministic_matches_oracle(name):
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    a.run(p.n // 2, SEED)  # start the snapshots from a non-trivial x (ASAGA steps)
+    st = oracle.sparse_saga(p, p.y, p.lam, g, SEED, p.n // 2)
+    x = st.x.copy()
+    a.set_algorithm("kromagnon")
+    with pytest.raises(m.AsagaError):
+        a.run(10, SEED)  # no snapshot yet
+    t = p.n // 2
+    for _ in range(2):
+        a.snapshot()
+        s, mu = oracle.svrg_snapshot(p, p.y, x)
+        _, alpha, ab, _ = a.get_state()
+        assert rel(alpha, s) <= 1e-12 and rel(ab, mu) <= 1e-11
+        oracle.svrg_inner(p, p.y, p.lam, g, SEED, t, p.n, s, mu, x)
+        a.run(p.n, SEED)
+        t += p.n
+        assert rel(a.get_state()[0], x) <= 1e-9
+
+
+@gpu
+def test_kromagnon_async_converges_hogwild_stalls():
+    """Fig. 1 qualitatively (P:455-461, P:540): async KROMAGNON reaches 1e-6 like ASAGA;
+    constant-step HOGWILD stalls at its variance floor."""
+    import json
+    import os
+
+    m = asaga_mod()
+    p = datagen.make("c1")
+    fstar = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fstar_c1.json")))["f_star"]
+    g = gamma_of(p)
+    k = m.Asaga.from_problem(p, g, concurrency=8)
+    k.set_algorithm("kromagnon")
+    for _ in range(15):
+        k.snapshot()
+        k.run(2 * p.n, SEED)
+    assert k.objective() - fstar <= 1e-6
+    h = m.Asaga.from_problem(p, g, concurrency=8)
+    h.set_algorithm("hogwild")
+    h.run(30 * p.n, SEED)
+    assert h.objective() - fstar > 1e-6
