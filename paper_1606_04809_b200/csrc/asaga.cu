@@ -951,10 +951,10 @@ int asaga_abi_version(void) { return ASAGA_ABI_VERSION; }
 
 #ifdef ASAGA_TIMING
 // Profiling build only: read and reset the per-phase cycle sums (not part of asaga.h).
-__attribute__((visibility("default"))) int asaga_debug_timing(unsigned long long* out6) {
+__attribute__((visibility("default"))) int asaga_debug_timing(unsigned long long* out9) {
   cudaDeviceSynchronize();
-  if (cudaMemcpyFromSymbol(out6, g_phase_cycles, 6 * sizeof(unsigned long long)) != cudaSuccess) return 1;
-  unsigned long long z[8] = {0};
+  if (cudaMemcpyFromSymbol(out9, g_phase_cycles, 9 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  unsigned long long z[12] = {0};
   cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
   return 0;
 }

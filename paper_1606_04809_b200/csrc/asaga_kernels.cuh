@@ -365,7 +365,7 @@ __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, c
 // Profiling build only (tools/timing_build.py): per-phase SM-cycle sums of group
 // leaders: [0] row wait, [1] gathers+dot, [2] reduce+exp, [3] scatter issue,
 // [4] loop tail, [5] iterations.
-__device__ unsigned long long g_phase_cycles[8];
+__device__ unsigned long long g_phase_cycles[12];
 #define TMARK(k)                                     \
   do {                                               \
     long long now_ = clock64();                      \
@@ -386,7 +386,7 @@ template <int G, int NR, bool DET, int MODE>
 __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   constexpr bool ATOMIC = MODE != 0;
 #ifdef ASAGA_TIMING
-  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
 #endif
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     // ---- pass 2: unlocked scatter (Property 3: atomic adds, no locks); row entries
     //      are re-read from the stage buffer, which is only overwritten next iteration
     if (MODE == 2) bulk_wait_read();  // the previous sample's bulk ops have read dbuf
+    TMARK(6);
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       if (lo + j * G >= hi) break;  // group-uniform
@@ -506,7 +507,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       }
     }
     if (MODE == 2) {
+      TMARK(7);
       fence_proxy_async_smem();
+      TMARK(8);
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
         if (lo + j * G >= hi) break;
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   }
 #ifdef ASAGA_TIMING
   if (g == 0)
-    for (int k = 0; k < 6; ++k) atomicAdd(&g_phase_cycles[k], ph[k]);
+    for (int k = 0; k < 9; ++k) atomicAdd(&g_phase_cycles[k], ph[k]);
 #endif
 }
 

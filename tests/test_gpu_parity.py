@@ -481,3 +481,38 @@ def test_kromagnon_async_converges_hogwild_stalls():
     h.set_algorithm("hogwild")
     h.run(30 * p.n, SEED)
     assert h.objective() - fstar > 1e-6
+
+
+@gpu
+def test_deterministic_c2_full_size_prefix():
+    """c2 at BASELINE full size (the bench workload): the first 1e5 updates match the oracle."""
+    p = datagen.make("c2")
+    _det_compare(p, 100_000, [50_000, 100_000])
+
+
+@gpu
+def test_bench_operating_point_c2_full_size_properties():
+    """c2 at full size in the bench's launch configuration (1024 in flight, gamma/8, bulk
+    scatter for features in >= 50% of rows): every sample processed once (bit-exact
+    histogram), the quiescent identity holds, f decreases monotonically over epochs."""
+    import scipy.sparse
+
+    import bench
+
+    m = asaga_mod()
+    p = datagen.make("c2")
+    W, gs, bulk = bench.OPERATING_POINT["c2"]
+    a = m.Asaga.from_problem(p, gs * gamma_of(p), concurrency=W, bulk_scatter_min_freq=bulk,
+                             record_samples=True)
+    fs = []
+    for _ in range(3):
+        a.run(p.n, SEED)
+        fs.append(a.objective())
+    assert fs[0] > fs[1] > fs[2]
+    ref = np.bincount(oracle.sample_stream(SEED, 0, 3 * p.n, p.n), minlength=p.n)
+    assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    # f at the GPU iterate, recomputed by the oracle, agrees with the GPU's A9 pass
+    assert fs[-1] == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)

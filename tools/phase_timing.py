@@ -43,8 +43,9 @@ def main():
               atomic=bool(args.atomic), lanes_per_sample=args.lanes,
               bulk_scatter_min_freq=args.bulk)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
-    buf = (ctypes.c_ulonglong * 6)()
-    names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail"]
+    buf = (ctypes.c_ulonglong * 9)()
+    names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail", "-", "s_wait_read", "s_compute",
+             "s_fence"]
     for W in [int(c) for c in args.conc.split(",")]:
         a.set_concurrency(W)
         a.run(p.n, 1)
@@ -53,9 +54,11 @@ def main():
         lib.asaga_debug_timing(buf)
         it = max(buf[5], 1)
         st = a.stats()
-        cyc = [buf[k] / it for k in range(5)]
-        print(f"{args.cfg} G={st['lanes_per_sample']} atomic={args.atomic} W={st['concurrency']} upd/s={p.n / st['last_run_ms'] * 1e3:.4g} "
-              f"cycles/sample total={sum(cyc):.0f}: " + " ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc)))
+        cyc = [buf[k] / it for k in range(9)]
+        # phases 6-8 split the scatter phase [3] (their sum is <= it: marks inside it)
+        print(f"{args.cfg} G={st['lanes_per_sample']} bulk={args.bulk} W={st['concurrency']} "
+              f"upd/s={p.n / st['last_run_ms'] * 1e3:.4g} cycles/sample total={sum(cyc[:5]):.0f}: "
+              + " ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc) if n != "-"))
 
 
 if __name__ == "__main__":
