@@ -105,6 +105,11 @@ typedef struct {
                             worker, and every k-th sample of a worker records the counter's
                             advance between its read and its write; mean / max in
                             asaga_stats.  0 (default) = off (no counter traffic). */
+  double hot_split_min_freq; /* features present in at least this fraction of rows keep
+                            abar_v in a separate array, so x_v and abar_v sit on different L2
+                            lines: each line then takes 2 operations per update (load + RED)
+                            instead of 3; one extra 8-byte gather per such entry.  0 (default)
+                            = off.  Exclusive with bulk_scatter_min_freq (ASAGA_E_INVALID_ARG). */
 } asaga_options;
 
 typedef struct {
@@ -124,6 +129,7 @@ typedef struct {
   int64_t overlap_max;    /* ... and the largest one */
   int64_t overlap_samples;
   int algorithm;          /* asaga_algorithm */
+  double hot_split_min_freq;
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

@@ -44,7 +44,7 @@ class Options(ctypes.Structure):
                 ("concurrency", ctypes.c_int64), ("lanes_per_sample", ctypes.c_int),
                 ("atomic_mode", ctypes.c_int), ("record_samples", ctypes.c_int),
                 ("stream", ctypes.c_void_p), ("bulk_scatter_min_freq", ctypes.c_double),
-                ("measure_overlap", ctypes.c_int)]
+                ("measure_overlap", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double)]
 
 
 class Stats(ctypes.Structure):
@@ -56,7 +56,7 @@ class Stats(ctypes.Structure):
                 ("grid", ctypes.c_int), ("block", ctypes.c_int), ("last_run_ms", ctypes.c_double),
                 ("bulk_scatter_min_freq", ctypes.c_double), ("overlap_mean", ctypes.c_double),
                 ("overlap_max", ctypes.c_int64), ("overlap_samples", ctypes.c_int64),
-                ("algorithm", ctypes.c_int)]
+                ("algorithm", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double)]
 
 
 ABI_FUNCTIONS = {
@@ -161,7 +161,8 @@ class Asaga:
     def __init__(self, indptr, indices, data, y, d: int, lam: float, gamma: float, *,
                  deterministic: bool = False, concurrency: int = 0, lanes_per_sample: int = 0,
                  atomic: bool = True, record_samples: bool = False, device: int = 0,
-                 stream=None, bulk_scatter_min_freq: float = 0.0, measure_overlap: int = 0):
+                 stream=None, bulk_scatter_min_freq: float = 0.0, measure_overlap: int = 0,
+                 hot_split_min_freq: float = 0.0):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -181,6 +182,7 @@ class Asaga:
         opt.stream = stream
         opt.bulk_scatter_min_freq = float(bulk_scatter_min_freq)
         opt.measure_overlap = int(measure_overlap)
+        opt.hot_split_min_freq = float(hot_split_min_freq)
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

@@ -54,6 +54,8 @@ struct asaga_ctx {
   double2* xa = nullptr;   // {x_v, abar_v} pairs at xa[v * S]
   int S = 1;               // pair stride
   double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
+  double hot_dmax = 0.0;   // hot split threshold on D_c (abar in habar)
+  double* habar = nullptr; // abar of hot-split features
   double* D = nullptr;     // reweighting n / n_v
   double* dv = nullptr;    // D_{c_k} per stored entry
   double* alpha = nullptr;  // folded alpha~ = b alpha
@@ -267,6 +269,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
 #endif
   TRY(dalloc(ctx, &ctx->xa, (size_t)d * ctx->S));
   TRY(dalloc(ctx, &ctx->D, d));
+  TRY(dalloc(ctx, &ctx->habar, d));
   TRY(dalloc(ctx, &ctx->dv, nnz));
   TRY(dalloc(ctx, &ctx->alpha, n));
   TRY(dalloc(ctx, &ctx->counts, d));
@@ -343,10 +346,11 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
   void* iargs[] = {&ip};
   CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
-  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->D, d, n,
+  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, d, n,
                                                                         ctx->flag + 1);
   CK(ctx, cudaGetLastError());
-  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(ctx->cols, ctx->D, nnz, ctx->dv);
+  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(ctx->cols, ctx->D, nnz,
+                                                                          ctx->hot_dmax, ctx->dv);
   CK(ctx, cudaGetLastError());
   unsigned long long h[ERR_COUNT + 2];
   int hmax_count = 0;
@@ -412,6 +416,13 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   }
   // p_v = n_v / n >= f  <=>  D_v = n / n_v <= 1 / f
   ctx->bulk_dmax = o.bulk_scatter_min_freq > 0.0 ? 1.0 / o.bulk_scatter_min_freq : 0.0;
+  if (!(o.hot_split_min_freq >= 0.0) || o.hot_split_min_freq > 1.0 ||
+      (o.hot_split_min_freq > 0.0 && o.bulk_scatter_min_freq > 0.0)) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG,
+                "hot_split_min_freq must be in [0, 1] and cannot be combined with bulk_scatter_min_freq");
+  }
+  ctx->hot_dmax = o.hot_split_min_freq > 0.0 ? 1.0 / o.hot_split_min_freq : 0.0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
   if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
@@ -566,6 +577,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.dv = ctx->dv;
   p.xa = ctx->xa;
   p.S = ctx->S;
+  p.habar = ctx->habar;
   p.alpha = ctx->alpha;
   p.visits = ctx->visits;
   p.ov = ctx->ov;
@@ -616,6 +628,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->measure_overlap = 0;
   opt->stream = nullptr;
   opt->bulk_scatter_min_freq = 0.0;
+  opt->hot_split_min_freq = 0.0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -763,7 +776,8 @@ asaga_status asaga_get_state(asaga_ctx* ctx, double* x, double* alpha, double* a
   cudaStream_t s = ctx->stream;
   if (x || alpha_bar) {
     unpack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
-        ctx->xa, ctx->S, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
+        ctx->xa, ctx->S, ctx->habar, ctx->D, ctx->hot_dmax, x ? ctx->tmp_d : nullptr,
+        alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
     CK(ctx, cudaGetLastError());
     if (x) CK(ctx, cudaMemcpyAsync(x, ctx->tmp_d, sizeof(double) * ctx->d, cudaMemcpyDeviceToHost, s));
     if (alpha_bar)
@@ -789,7 +803,7 @@ asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alph
     CK(ctx, cudaMemcpyAsync(ctx->tmp_d2, alpha_bar, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
   if (x || alpha_bar) {
     pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
-        ctx->xa, ctx->S, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
+        ctx->xa, ctx->S, ctx->habar, x ? ctx->tmp_d : nullptr, alpha_bar ? ctx->tmp_d2 : nullptr, ctx->d);
     CK(ctx, cudaGetLastError());
   }
   if (alpha) {
@@ -859,6 +873,7 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->last_run_ms = ctx->last_ms;
   out->bulk_scatter_min_freq = ctx->bulk_dmax > 0.0 ? 1.0 / ctx->bulk_dmax : 0.0;
   out->algorithm = ctx->algorithm;
+  out->hot_split_min_freq = ctx->hot_dmax > 0.0 ? 1.0 / ctx->hot_dmax : 0.0;
   out->overlap_mean = 0.0;
   out->overlap_max = 0;
   out->overlap_samples = 0;
@@ -916,8 +931,8 @@ asaga_status asaga_set_algorithm(asaga_ctx* ctx, int algorithm) {
   if (algorithm == ASAGA_ALG_HOGWILD) {  // HOGWILD's memory is identically zero
     CK(ctx, cudaMemsetAsync(ctx->alpha, 0, sizeof(double) * ctx->n, ctx->stream));
     CK(ctx, cudaMemsetAsync(ctx->tmp_d2, 0, sizeof(double) * ctx->d, ctx->stream));
-    pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->xa, ctx->S, nullptr,
-                                                                              ctx->tmp_d2, ctx->d);
+    pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, ctx->stream>>>(ctx->xa, ctx->S, ctx->habar,
+                                                                              nullptr, ctx->tmp_d2, ctx->d);
     CK(ctx, cudaGetLastError());
     CK(ctx, cudaStreamSynchronize(ctx->stream));
   }
@@ -939,8 +954,8 @@ asaga_status asaga_snapshot(asaga_ctx* ctx) {
   asaga_status st = enqueue_gradient(ctx, current_x(ctx), current_xs(ctx), ctx->tmp_d2, 1, s);
   ctx->lambda = lam;
   TRY(st);
-  pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->xa, ctx->S, nullptr, ctx->tmp_d2,
-                                                                  ctx->d);
+  pack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(ctx->xa, ctx->S, ctx->habar, nullptr,
+                                                                  ctx->tmp_d2, ctx->d);
   CK(ctx, cudaGetLastError());
   CK(ctx, cudaStreamSynchronize(s));
   ctx->snapshot_valid = true;

@@ -227,13 +227,14 @@ __global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
 
 // A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
 __global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa,
-                               int S, double* __restrict__ D, int64_t d, int64_t n,
-                               int* __restrict__ max_count) {
+                               int S, double* __restrict__ habar, double* __restrict__ D, int64_t d,
+                               int64_t n, int* __restrict__ max_count) {
   int my = 0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int c = counts[v];
     xa[v * S] = make_double2(0.0, 0.0);
+    habar[v] = 0.0;
     D[v] = c > 0 ? (double)n / (double)c : 0.0;
     my = max(my, c);
   }
@@ -242,11 +243,16 @@ __global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __re
 }
 
 // A1: dv[k] = D[cols[k]] (the row stream carries D; see the layout note above).
+// Hot split (hot_dmax > 0): an entry of a popular feature (D_c <= hot_dmax, i.e.
+// p_c >= 1/hot_dmax) carries -D_c: its abar lives in the separate `habar` array, so
+// x_c and abar_c sit on different L2 lines (2 operations per line per update, not 3).
 __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* __restrict__ D,
-                                int64_t nnz, double* __restrict__ dv) {
+                                int64_t nnz, double hot_dmax, double* __restrict__ dv) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
-       k += (int64_t)gridDim.x * blockDim.x)
-    dv[k] = __ldg(D + cols[k]);
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double Dc = __ldg(D + cols[k]);
+    dv[k] = (hot_dmax > 0.0 && Dc <= hot_dmax) ? -Dc : Dc;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -277,6 +283,7 @@ struct UpdateParams {
   const double* dv;     // D_{c_k} per stored entry
   double2* xa;          // {x_v, abar_v} at xa[v * S]
   int S;                // pair stride
+  double* habar;        // abar_v of hot-split features (entries with dv < 0)
   double* alpha;        // folded alpha~
   int32_t* visits;      // NULL unless record_samples
   unsigned long long* ov;  // NULL, or overlap instrumentation (NEXT-1, App. D):
@@ -440,12 +447,23 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     for (int j = 0; j < NR; ++j) {
       if (lo + j * G >= hi) break;  // group-uniform
       const int64_t k = lo + j * G + g;
-      if (k < hi) xb[j] = ld_na2(p.xa + (int64_t)sc[j * G + g] * p.S);
+      if (k < hi) {
+        const int c = sc[j * G + g];
+        if (sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
+          xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c));
+        else
+          xb[j] = ld_na2(p.xa + (int64_t)c * p.S);
+      }
     }
     const double ai = ld_na(p.alpha + i);
     // ---- look-ahead (read-only data): copy row t+W, load bounds of t+2W
     const bool has1 = t + W < tend, has2 = t + 2 * W < tend;
-    if (has1) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
+#ifdef ASAGA_TIMING
+    const bool copy_late = (p.debug_mode & 4) != 0;
+#else
+    constexpr bool copy_late = false;
+#endif
+    if (has1 && !copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
     int64_t lo2 = 0, hi2 = 0;
     if (has2) {
       lo2 = __ldg(&p.rowptr[in2]);
@@ -458,16 +476,19 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const int64_t k = lo + j * G + g;
       if (k < hi) {
         dot = fma(sv[j * G + g], xb[j].x, dot);
-        qq[j] = sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
+        qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
       }
     }
     for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
-      const double2 v = ld_na2(p.xa + (int64_t)c * p.S);
+      const double Dv = ld_nc_f64(p.dv + k);
+      const double2 v = Dv < 0.0 ? make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c))
+                                 : ld_na2(p.xa + (int64_t)c * p.S);
       dot = fma(a, v.x, dot);
-      qs[k - lo - P] = ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
+      qs[k - lo - P] = fabs(Dv) * fma(p.lambda_, v.x, v.y);
     }
+    if (has1 && copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
     TMARK(1);
     // ---- scalar derivative (folded logistic) and memory difference
     dot = group_sum<G>(dot, gmask);
@@ -495,14 +516,15 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         const double a = sv[j * G + g];
         const double u = fma(da, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
+        double* abv = sd[j * G + g] < 0.0 ? p.habar + c : xv + 1;  // hot split
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
           dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : da * a * p.inv_n);
         } else if (MODE >= 1) {
           red_add(xv, ngam * u);
-          if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+          if (!p.frozen) red_add(abv, da * a * p.inv_n);
         } else {
           st_cg(xv, ld_cg(xv) + ngam * u);
-          if (!p.frozen) st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
+          if (!p.frozen) st_cg(abv, ld_cg(abv) + da * a * p.inv_n);
         }
       }
     }
@@ -524,12 +546,13 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const double a = ld_nc_f64(p.vals + k);
       const double u = fma(da, a, qs[k - lo - P]);
       double* xv = &p.xa[(int64_t)c * p.S].x;
+      double* abv = ld_nc_f64(p.dv + k) < 0.0 ? p.habar + c : xv + 1;  // hot split
       if (ATOMIC) {
         red_add(xv, ngam * u);
-        if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+        if (!p.frozen) red_add(abv, da * a * p.inv_n);
       } else {
         st_cg(xv, ld_cg(xv) + ngam * u);
-        if (!p.frozen) st_cg(xv + 1, ld_cg(xv + 1) + da * a * p.inv_n);
+        if (!p.frozen) st_cg(abv, ld_cg(abv) + da * a * p.inv_n);
       }
     }
 #ifdef ASAGA_TIMING
@@ -757,21 +780,27 @@ __global__ void fold_alpha_kernel(const double* __restrict__ in, const double* _
     out[i] = y[i] * in[i];
 }
 
-__global__ void unpack_xa_kernel(const double2* __restrict__ xa, int S, double* __restrict__ x,
-                                 double* __restrict__ ab, int64_t d) {
+// abar_v lives in habar[v] for hot-split features (D_v <= hot_dmax), else in xa[v*S].y
+__global__ void unpack_xa_kernel(const double2* __restrict__ xa, int S, const double* __restrict__ habar,
+                                 const double* __restrict__ D, double hot_dmax,
+                                 double* __restrict__ x, double* __restrict__ ab, int64_t d) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     if (x) x[v] = xa[v * S].x;
-    if (ab) ab[v] = xa[v * S].y;
+    if (ab) ab[v] = (hot_dmax > 0.0 && D[v] <= hot_dmax) ? habar[v] : xa[v * S].y;
   }
 }
 
-__global__ void pack_xa_kernel(double2* __restrict__ xa, int S, const double* __restrict__ x,
-                               const double* __restrict__ ab, int64_t d) {
+// writes abar to both homes (the pair slot and habar): correct whatever the split
+__global__ void pack_xa_kernel(double2* __restrict__ xa, int S, double* __restrict__ habar,
+                               const double* __restrict__ x, const double* __restrict__ ab, int64_t d) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     if (x) xa[v * S].x = x[v];
-    if (ab) xa[v * S].y = ab[v];
+    if (ab) {
+      xa[v * S].y = ab[v];
+      habar[v] = ab[v];
+    }
   }
 }
 

@@ -75,11 +75,11 @@ def test_sampler_bitexact(n, seed, t0):
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
-def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0):
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0):
     m = asaga_mod()
     g = gamma_of(prob)
     a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
-                             bulk_scatter_min_freq=bulk)
+                             bulk_scatter_min_freq=bulk, hot_split_min_freq=split)
     st = oracle.State(prob.n, prob.d)
     D = oracle.reweight(prob.n, oracle.column_counts(prob))
     done = 0
@@ -119,6 +119,14 @@ def test_deterministic_lane_groupings(lanes):
 def test_deterministic_bulk_scatter(name, bulk):
     """The TMA bulk pair reduction (all features, or the popular ones) is the same arithmetic."""
     _det_compare(SUBSETS[name](), 20_000, [1, 5_000, 20_000], bulk=bulk)
+
+
+@gpu
+@pytest.mark.parametrize("split", [1e-300, 0.3])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_deterministic_hot_split(name, split):
+    """abar of popular features in its own array (x and abar on separate lines): same arithmetic."""
+    _det_compare(SUBSETS[name](), 20_000, [1, 5_000, 20_000], split=split)
 
 
 @gpu
@@ -267,9 +275,9 @@ def test_async_c1_epochs_within_1p5x_oracle(conc):
 
 
 @gpu
-@pytest.mark.parametrize("bulk", [0.0, 0.5, 1e-300])
+@pytest.mark.parametrize("bulk,split", [(0.0, 0.0), (0.5, 0.0), (1e-300, 0.0), (0.0, 0.3), (0.0, 1e-300)])
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
-def test_async_sample_stream_and_quiescent_identity(name, bulk):
+def test_async_sample_stream_and_quiescent_identity(name, bulk, split):
     """Every t is processed exactly once (visit histogram == oracle's stream histogram,
     bit-exact) and, once quiescent, abar == (1/n) sum alpha_i a_i (no lost update)."""
     import scipy.sparse
@@ -277,7 +285,8 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk):
     m = asaga_mod()
     p = SUBSETS[name]()
     T = 5 * p.n + 12345
-    a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True, bulk_scatter_min_freq=bulk)
+    a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True, bulk_scatter_min_freq=bulk,
+                             hot_split_min_freq=split)
     a.run(T, SEED)
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
@@ -359,6 +368,10 @@ def test_errors():
             mk(**kw)
         assert ei.value.name == name, (kw, ei.value)
         assert frag in str(ei.value), (kw, ei.value)
+    with pytest.raises(E) as ei:
+        m.Asaga(ok["indptr"], ok["indices"], ok["data"], ok["y"], 2, 0.5, 1.0,
+                bulk_scatter_min_freq=0.5, hot_split_min_freq=0.5)
+    assert ei.value.name == "ASAGA_E_INVALID_ARG"
     a = mk()
     with pytest.raises(E) as ei:
         a.sample_counts()
@@ -421,12 +434,13 @@ def test_overlap_estimate_tracks_samples_in_flight():
 
 # ---------------------------------------------------------------------- NEXT-2 comparison methods
 @gpu
+@pytest.mark.parametrize("split", [0.0, 0.3])
 @pytest.mark.parametrize("name", ["c1", "c3s"])
-def test_hogwild_deterministic_matches_oracle(name):
+def test_hogwild_deterministic_matches_oracle(name, split):
     m = asaga_mod()
     p = SUBSETS[name]()
     g = gamma_of(p)
-    a = m.Asaga.from_problem(p, g, deterministic=True)
+    a = m.Asaga.from_problem(p, g, deterministic=True, hot_split_min_freq=split)
     a.set_algorithm("hogwild")
     a.run(3 * p.n, SEED)
     x, alpha, ab, _ = a.get_state()
@@ -436,12 +450,13 @@ def test_hogwild_deterministic_matches_oracle(name):
 
 
 @gpu
+@pytest.mark.parametrize("split", [0.0, 0.3])
 @pytest.mark.parametrize("name", ["c1", "c3s"])
-def test_kromagnon_deterministic_matches_oracle(name):
+def test_kromagnon_deterministic_matches_oracle(name, split):
     m = asaga_mod()
     p = SUBSETS[name]()
     g = gamma_of(p)
-    a = m.Asaga.from_problem(p, g, deterministic=True)
+    a = m.Asaga.from_problem(p, g, deterministic=True, hot_split_min_freq=split)
     a.run(p.n // 2, SEED)  # start the snapshots from a non-trivial x (ASAGA steps)
     st = oracle.sparse_saga(p, p.y, p.lam, g, SEED, p.n // 2)
     x = st.x.copy()

@@ -136,6 +136,36 @@ __global__ void k_bulk_pair(double* tab, uint32_t k, uint32_t d, int iters, int 
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// latency of one "sample's" gathers: a warp issues NCH x 32-lane scattered 16-byte
+// .na loads (a row of NCH*32 entries), waits, and derives the next addresses from
+// the data -- cycles per round, one warp per SM (the W = 148 regime)
+__global__ void k_gather_lat(const double2* tab, uint32_t d, int nch, int rounds,
+                             unsigned long long* out) {
+  const int lane = threadIdx.x & 31;
+  uint32_t seed = blockIdx.x * 7919u + lane;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int r = 0; r < rounds; ++r) {
+    double2 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < nch) {
+        uint32_t c = hash32(seed + j * 131u + r * 977u) % d;
+        asm volatile("ld.global.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(v[j].x), "=d"(v[j].y) : "l"(tab + c) : "memory");
+      } else {
+        v[j] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc += v[j].x + v[j].y;
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    seed += (uint32_t)(acc == 1.2345 ? 1 : 0);  // true data dependence of the next round
+  }
+  long long t1 = clock64();
+  if (lane == 0) atomicAdd(out, (unsigned long long)(t1 - t0));
+  if (acc == 1.2345) out[1] = 1;  // keep the loads
+}
+
 __global__ void k_red_list(double* tab, const uint32_t* __restrict__ list, uint64_t m, uint32_t stride) {
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (uint64_t)gridDim.x * blockDim.x)
     asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(tab + (size_t)__ldg(list + j) * stride), "d"(1.0) : "memory");
@@ -336,6 +366,31 @@ int main(int argc, char** argv) {
              g_hot / ms_hot * 1e3 / 10, g_rnd / ms_rnd * 1e3);
     js += buf;
     CK(cudaFree(tab));
+  }
+  // M2b latency of a sample's gathers (one warp per SM)
+  {
+    const uint32_t d = 47236;
+    double2* tab;
+    unsigned long long* acc;
+    CK(cudaMalloc(&tab, (size_t)d * 16));
+    CK(cudaMemset(tab, 0, (size_t)d * 16));
+    CK(cudaMalloc(&acc, 16));
+    js += ", \"gather_latency_cycles\": {";
+    for (int nch = 1; nch <= 4; ++nch) {
+      const int rounds = 2000;
+      k_gather_lat<<<sms, 32>>>(tab, d, nch, 50, acc);  // warm
+      CK(cudaMemset(acc, 0, 8));
+      k_gather_lat<<<sms, 32>>>(tab, d, nch, rounds, acc);
+      CK(cudaGetLastError());
+      CK(cudaDeviceSynchronize());
+      unsigned long long h = 0;
+      CK(cudaMemcpy(&h, acc, 8, cudaMemcpyDeviceToHost));
+      snprintf(buf, sizeof buf, "%s\"chunks%d\": %.1f", nch == 1 ? "" : ", ", nch, (double)h / sms / rounds);
+      js += buf;
+    }
+    js += "}";
+    CK(cudaFree(tab));
+    CK(cudaFree(acc));
   }
   // M5 Zipf RED pattern
   {
