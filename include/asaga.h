@@ -110,6 +110,12 @@ typedef struct {
                             lines: each line then takes 2 operations per update (load + RED)
                             instead of 3; one extra 8-byte gather per such entry.  0 (default)
                             = off.  Exclusive with bulk_scatter_min_freq (ASAGA_E_INVALID_ARG). */
+  int smem_replica_refresh; /* r > 0 and d <= 4096, async mode: every thread block keeps a
+                            shared-memory replica of all {x_v, abar_v}; gathers read it, writes
+                            still go to the shared state, and each worker refreshes G replica
+                            entries from L2 every r samples.  Reads become older but stay
+                            bounded-delay inconsistent reads (Assumption 1).
+                            0 (default) = off. */
 } asaga_options;
 
 typedef struct {
@@ -130,6 +136,7 @@ typedef struct {
   int64_t overlap_samples;
   int algorithm;          /* asaga_algorithm */
   double hot_split_min_freq;
+  int smem_replica;       /* 1 when the shared-memory replica is in use */
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

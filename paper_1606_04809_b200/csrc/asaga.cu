@@ -55,6 +55,7 @@ struct asaga_ctx {
   int S = 1;               // pair stride
   double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
   double hot_dmax = 0.0;   // hot split threshold on D_c (abar in habar)
+  int replica_every = 0;   // > 0: shared-memory replica of {x, abar} (small d, async)
   double* habar = nullptr; // abar of hot-split features
   double* D = nullptr;     // reweighting n / n_v
   double* dv = nullptr;    // D_{c_k} per stored entry
@@ -156,41 +157,55 @@ int grid_for(const asaga_ctx* ctx, int64_t work, int block) {
 
 using UpdFn = void (*)(UpdateParams);
 
-template <int G, int NR, bool DET>
+template <int G, int NR, bool DET, bool REPL>
 UpdFn pick_mode(int mode) {
   switch (mode) {
-    case 0: return asaga_update_kernel<G, NR, DET, 0>;
-    case 2: return asaga_update_kernel<G, NR, DET, 2>;
-    default: return asaga_update_kernel<G, NR, DET, 1>;
+    case 0: return asaga_update_kernel<G, NR, DET, 0, REPL>;
+    case 2: return asaga_update_kernel<G, NR, DET, 2, REPL>;
+    default: return asaga_update_kernel<G, NR, DET, 1, REPL>;
   }
 }
 
 template <int G, int NR>
-UpdFn pick_upd(bool det, int mode) {
-  return det ? pick_mode<G, NR, true>(mode) : pick_mode<G, NR, false>(mode);
+UpdFn pick_upd(bool det, int mode, bool repl) {
+  if (det) return pick_mode<G, NR, true, false>(mode);  // deterministic mode reads L2 directly
+  return repl ? pick_mode<G, NR, false, true>(mode) : pick_mode<G, NR, false, false>(mode);
 }
 
 template <int G>
-UpdFn pick_upd_nr(int nr, bool det, int mode) {
+UpdFn pick_upd_nr(int nr, bool det, int mode, bool repl) {
   switch (nr) {
-    case 1: return pick_upd<G, 1>(det, mode);
-    case 2: return pick_upd<G, 2>(det, mode);
-    case 4: return pick_upd<G, 4>(det, mode);
-    default: return pick_upd<G, 8>(det, mode);
+    case 1: return pick_upd<G, 1>(det, mode, repl);
+    case 2: return pick_upd<G, 2>(det, mode, repl);
+    case 4: return pick_upd<G, 4>(det, mode, repl);
+    default: return pick_upd<G, 8>(det, mode, repl);
   }
 }
 
 // scatter mode: 0 non-atomic ablation, 1 LSU REDs, 2 TMA bulk pair reductions
 int scatter_mode(const asaga_ctx* ctx);
 
+bool use_replica(const asaga_ctx* ctx);
+
 UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
   const bool det = ctx->deterministic != 0;
   const int mode = scatter_mode(ctx);
+  const bool repl = use_replica(ctx);
   switch (lanes) {
-    case 8: return pick_upd_nr<8>(nr, det, mode);
-    case 16: return pick_upd_nr<16>(nr, det, mode);
-    default: return pick_upd_nr<32>(nr, det, mode);
+    case 8: return pick_upd_nr<8>(nr, det, mode, repl);
+    case 16: return pick_upd_nr<16>(nr, det, mode, repl);
+    default: return pick_upd_nr<32>(nr, det, mode, repl);
   }
+}
+
+constexpr int64_t kReplicaMaxD = 4096;  // 64 KiB of {x, abar} pairs per block
+
+bool use_replica(const asaga_ctx* ctx) {
+  return ctx->replica_every > 0 && !ctx->deterministic && ctx->d <= kReplicaMaxD;
+}
+
+size_t replica_bytes(const asaga_ctx* ctx) {
+  return use_replica(ctx) ? (((size_t)ctx->d * 16 + 15) & ~(size_t)15) : 0;
 }
 
 int scatter_mode(const asaga_ctx* ctx) {
@@ -233,7 +248,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
                              2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
                              (size_t)ctx->overflow * sizeof(double);
   ctx->group_bytes = group_bytes;
-  ctx->smem = (size_t)groups_per_block * group_bytes;
+  ctx->smem = replica_bytes(ctx) + (size_t)groups_per_block * group_bytes;
   UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 227 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
@@ -423,6 +438,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
                 "hot_split_min_freq must be in [0, 1] and cannot be combined with bulk_scatter_min_freq");
   }
   ctx->hot_dmax = o.hot_split_min_freq > 0.0 ? 1.0 / o.hot_split_min_freq : 0.0;
+  ctx->replica_every = o.smem_replica_refresh > 0 ? o.smem_replica_refresh : 0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
   if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
@@ -582,6 +598,8 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.visits = ctx->visits;
   p.ov = ctx->ov;
   p.frozen = ctx->algorithm != ASAGA_ALG_ASAGA ? 1 : 0;
+  p.repl_d = use_replica(ctx) ? (int)ctx->d : 0;
+  p.repl_every = ctx->replica_every > 0 ? ctx->replica_every : 1;
   p.ov_every = ctx->ov_every > 0 ? ctx->ov_every : 1;
   p.n = (uint64_t)ctx->n;
   p.gamma = ctx->gamma;
@@ -603,7 +621,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
   int grid = 1, block = 32;
   launch_shape(ctx, workers, &grid, &block);
-  const size_t smem = (size_t)(block / ctx->lanes) * ctx->group_bytes;
+  const size_t smem = replica_bytes(ctx) + (size_t)(block / ctx->lanes) * ctx->group_bytes;
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   void* args[] = {&p};
   CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(block), args, smem, ctx->stream));
@@ -629,6 +647,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->stream = nullptr;
   opt->bulk_scatter_min_freq = 0.0;
   opt->hot_split_min_freq = 0.0;
+  opt->smem_replica_refresh = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -874,6 +893,7 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->bulk_scatter_min_freq = ctx->bulk_dmax > 0.0 ? 1.0 / ctx->bulk_dmax : 0.0;
   out->algorithm = ctx->algorithm;
   out->hot_split_min_freq = ctx->hot_dmax > 0.0 ? 1.0 / ctx->hot_dmax : 0.0;
+  out->smem_replica = use_replica(ctx) ? 1 : 0;
   out->overlap_mean = 0.0;
   out->overlap_max = 0;
   out->overlap_samples = 0;

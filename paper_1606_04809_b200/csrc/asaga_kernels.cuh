@@ -290,6 +290,8 @@ struct UpdateParams {
                            // [0] sparse global progress counter (+100 per 100 local samples),
                            // [1] sum and [2] count of per-sample overlap estimates, [3] max
   int ov_every;            // measure every ov_every-th local sample
+  int repl_d;              // REPL: features held in the per-CTA shared-memory replica (= d)
+  int repl_every;          // REPL: a group refreshes G replica entries every repl_every samples
   int frozen;              // 1: the memory (alpha, abar) is read but never written --
                            // KROMAGNON inner steps (alpha = sigma(x~), abar = mu) and
                            // HOGWILD (alpha = abar = 0), NEXT-2
@@ -389,7 +391,13 @@ __device__ unsigned long long g_phase_cycles[12];
 // element (LSU), 2 = hybrid: one TMA bulk 16-byte reduction per {x, abar} pair of
 // a popular feature (D_c <= bulk_dmax: its L2 line is the bottleneck), REDs for the
 // rest (the bulk op is issued lane by lane, ~64 cycles each).
-template <int G, int NR, bool DET, int MODE>
+// REPL (small d, async only): every CTA keeps a shared-memory replica of all {x_v, abar_v}
+// pairs; gathers read the replica (30-cycle LDS instead of an L2 round trip on the hot
+// lines) while every write still goes to the shared state in L2.  Each group refreshes G
+// replica entries from L2 every repl_every samples, so a replica value is a past value of
+// the shared state of bounded age: the reads stay the paper's inconsistent reads (P:137,
+// P:266-268) with a larger, still bounded, overlap (Assumption 1).
+template <int G, int NR, bool DET, int MODE, bool REPL>
 __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   constexpr bool ATOMIC = MODE != 0;
 #ifdef ASAGA_TIMING
@@ -403,8 +411,17 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   const unsigned gmask =
       (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  double2* rx = reinterpret_cast<double2*>(smem_raw);  // REPL replica (first in smem)
+  const size_t repl_bytes = REPL ? (((size_t)p.repl_d * sizeof(double2) + 15) & ~(size_t)15) : 0;
+  if (REPL) {  // fill before any early exit: the whole block takes part in the barrier
+    for (int v = threadIdx.x; v < p.repl_d; v += blockDim.x) rx[v] = ld_na2(p.xa + (int64_t)v * p.S);
+    __syncthreads();
+  }
   if (w >= p.workers) return;
-  unsigned char* gbase = smem_raw + (size_t)(threadIdx.x / G) * GroupSmem<G, NR>::bytes(p.overflow);
+  unsigned char* gbase =
+      smem_raw + repl_bytes + (size_t)(threadIdx.x / G) * GroupSmem<G, NR>::bytes(p.overflow);
+  int rcur = REPL ? (int)(((threadIdx.x / G) * G) % (p.repl_d > 0 ? p.repl_d : 1)) : 0;
+  int rtick = 0;
   double2* dbuf = reinterpret_cast<double2*>(gbase);
   double* qs = reinterpret_cast<double*>(gbase + GroupSmem<G, NR>::delta_bytes +
                                          2 * GroupSmem<G, NR>::stage_bytes);
@@ -449,13 +466,24 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const int64_t k = lo + j * G + g;
       if (k < hi) {
         const int c = sc[j * G + g];
-        if (sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
+        if (REPL)
+          xb[j] = rx[c];
+        else if (sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
           xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c));
         else
           xb[j] = ld_na2(p.xa + (int64_t)c * p.S);
       }
     }
     const double ai = ld_na(p.alpha + i);
+    // REPL: refresh G replica entries from the shared state every repl_every samples
+    const bool refresh = REPL && (++rtick >= p.repl_every);
+    double2 rv = make_double2(0.0, 0.0);
+    int rf = 0;
+    if (refresh) {
+      rf = rcur + g;
+      if (rf >= p.repl_d) rf -= p.repl_d;
+      if (g < p.repl_d) rv = ld_na2(p.xa + (int64_t)rf * p.S);
+    }
     // ---- look-ahead (read-only data): copy row t+W, load bounds of t+2W
     const bool has1 = t + W < tend, has2 = t + 2 * W < tend;
 #ifdef ASAGA_TIMING
@@ -483,8 +511,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
       const double Dv = ld_nc_f64(p.dv + k);
-      const double2 v = Dv < 0.0 ? make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c))
-                                 : ld_na2(p.xa + (int64_t)c * p.S);
+      const double2 v = REPL ? rx[c]
+                        : Dv < 0.0 ? make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c))
+                                   : ld_na2(p.xa + (int64_t)c * p.S);
       dot = fma(a, v.x, dot);
       qs[k - lo - P] = fabs(Dv) * fma(p.lambda_, v.x, v.y);
     }
@@ -558,6 +587,12 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #ifdef ASAGA_TIMING
     }
 #endif
+    if (refresh) {
+      if (g < p.repl_d) rx[rf] = rv;
+      rcur += G;
+      if (rcur >= p.repl_d) rcur -= p.repl_d;
+      rtick = 0;
+    }
     TMARK(3);
     if (g == 0) {
       if (p.frozen) {

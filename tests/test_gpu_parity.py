@@ -250,8 +250,8 @@ def _epochs_to(p, f_star, runner, tol=1e-6, max_epochs=60):
 
 
 @gpu
-@pytest.mark.parametrize("conc", [1, 4, 16])
-def test_async_c1_epochs_within_1p5x_oracle(conc):
+@pytest.mark.parametrize("conc,repl", [(1, 0), (4, 0), (16, 0), (16, 1), (64, 4)])
+def test_async_c1_epochs_within_1p5x_oracle(conc, repl):
     m = asaga_mod()
     p = datagen.make("c1")
     fs = _fstar(p)
@@ -264,7 +264,7 @@ def test_async_c1_epochs_within_1p5x_oracle(conc):
         return oracle.objective(p, p.y, p.lam, st.x)
 
     e_or = _epochs_to(p, fs, orun)
-    a = m.Asaga.from_problem(p, g, concurrency=conc)
+    a = m.Asaga.from_problem(p, g, concurrency=conc, smem_replica_refresh=repl)
 
     def grun(k):
         a.run(k, SEED)
@@ -275,9 +275,10 @@ def test_async_c1_epochs_within_1p5x_oracle(conc):
 
 
 @gpu
-@pytest.mark.parametrize("bulk,split", [(0.0, 0.0), (0.5, 0.0), (1e-300, 0.0), (0.0, 0.3), (0.0, 1e-300)])
+@pytest.mark.parametrize("bulk,split,repl", [(0.0, 0.0, 0), (0.5, 0.0, 0), (1e-300, 0.0, 0), (0.0, 0.3, 0),
+                                             (0.0, 1e-300, 0), (0.0, 0.0, 1), (0.5, 0.0, 4)])
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
-def test_async_sample_stream_and_quiescent_identity(name, bulk, split):
+def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl):
     """Every t is processed exactly once (visit histogram == oracle's stream histogram,
     bit-exact) and, once quiescent, abar == (1/n) sum alpha_i a_i (no lost update)."""
     import scipy.sparse
@@ -286,7 +287,8 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split):
     p = SUBSETS[name]()
     T = 5 * p.n + 12345
     a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True, bulk_scatter_min_freq=bulk,
-                             hot_split_min_freq=split)
+                             hot_split_min_freq=split, smem_replica_refresh=repl)
+    assert a.stats()["smem_replica"] == (1 if repl and p.d <= 4096 else 0)
     a.run(T, SEED)
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)

@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--every", type=int, default=8)
     ap.add_argument("--bulk", type=float, default=0.0)
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
+    ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -35,7 +36,8 @@ def main():
     for W in [int(c) for c in args.conc.split(",")]:
         a = Asaga(*A, p.d, p.lam, 1.0, concurrency=W, measure_overlap=args.every,
                   bulk_scatter_min_freq=args.bulk,
-              hot_split_min_freq=args.split)
+              hot_split_min_freq=args.split,
+              smem_replica_refresh=args.repl)
         a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
         T = int(args.epochs * p.n)
         a.run(T, datagen.SAMPLE_SEED)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
+    ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     args = ap.parse_args()
     import importlib.util
 
@@ -43,7 +44,8 @@ def main():
     a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0,
               atomic=bool(args.atomic), lanes_per_sample=args.lanes,
               bulk_scatter_min_freq=args.bulk,
-              hot_split_min_freq=args.split)
+              hot_split_min_freq=args.split,
+              smem_replica_refresh=args.repl)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     buf = (ctypes.c_ulonglong * 9)()
     names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail", "-", "s_wait_read", "s_compute",
@@ -58,7 +60,7 @@ def main():
         st = a.stats()
         cyc = [buf[k] / it for k in range(9)]
         # phases 6-8 split the scatter phase [3] (their sum is <= it: marks inside it)
-        print(f"{args.cfg} G={st['lanes_per_sample']} bulk={args.bulk} split={args.split} W={st['concurrency']} "
+        print(f"{args.cfg} G={st['lanes_per_sample']} bulk={args.bulk} split={args.split} repl={args.repl} W={st['concurrency']} "
               f"upd/s={p.n / st['last_run_ms'] * 1e3:.4g} cycles/sample total={sum(cyc[:5]):.0f}: "
               + " ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc) if n != "-"))
 

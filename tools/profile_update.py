@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--updates", type=int, default=0, help="default: one epoch")
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
+    ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -29,7 +30,8 @@ def main():
     t = lambda a: torch.from_numpy(a).to(dev)
     a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc,
               bulk_scatter_min_freq=args.bulk,
-              hot_split_min_freq=args.split)
+              hot_split_min_freq=args.split,
+              smem_replica_refresh=args.repl)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     T = args.updates or p.n
     a.run(T, datagen.SAMPLE_SEED)  # warm-up launch

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
+    ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -43,7 +44,8 @@ def main():
     t = lambda a: torch.from_numpy(a).to(dev)
     A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
     base = Asaga(*A, p.d, p.lam, 1.0, bulk_scatter_min_freq=args.bulk,
-              hot_split_min_freq=args.split)
+              hot_split_min_freq=args.split,
+              smem_replica_refresh=args.repl)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     for W in [int(c) for c in args.conc.split(",")]:
