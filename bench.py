@@ -38,8 +38,12 @@ import datagen  # noqa: E402
 # Convergent operating points (W samples in flight, gamma scale vs 1/(3L), bulk-scatter
 # feature frequency) from tools/sweep.py on B200 (profiles/r01_operating_point.md):
 # the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
-OPERATING_POINT = {"c1": (16, 1.0, 0.0), "c2": (1024, 0.125, 0.5), "c3": (256, 0.35, 0.0),
-                   "c4": (256, 0.25, 0.0)}
+OPERATING_POINT = {
+    "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0),
+    "c2": dict(W=1024, gscale=0.125, bulk=0.5, split=0.0, repl=1),
+    "c3": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0),
+    "c4": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0),
+}
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -221,15 +225,17 @@ def main():
     from paper_1606_04809_b200 import Asaga
 
     p = datagen.make(args.workload)
-    W0, gs0, bulk = OPERATING_POINT[args.workload]
-    W = args.concurrency if args.concurrency is not None else W0
-    gscale = args.gamma_scale if args.gamma_scale is not None else gs0
+    op = OPERATING_POINT[args.workload]
+    W = args.concurrency if args.concurrency is not None else op["W"]
+    gscale = args.gamma_scale if args.gamma_scale is not None else op["gscale"]
+    bulk = op["bulk"]
     lam = p.lam * (10.0 ** (-rank))  # rank 0: lambda = 1/n (the BASELINE config)
     dev = torch.device("cuda", local)
     t = lambda arr: torch.from_numpy(arr).to(dev)
     indptr, indices, data, y = t(p.indptr), t(p.indices), t(p.data), t(p.y)
     a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local,
-              bulk_scatter_min_freq=bulk)
+              bulk_scatter_min_freq=bulk, hot_split_min_freq=op["split"],
+              smem_replica_refresh=op["repl"])
     L = a.stats()["L"]
     gamma = gscale / (3.0 * L)
     a.set_gamma(gamma)
@@ -311,8 +317,18 @@ def main():
         upd_avg_s = float(np.mean(upd_ms)) / 1e3
         ups = p.n / upd_avg_s
         achieved = bpu * p.n / upd_avg_s / 1e9
+        # the ceiling of the hottest feature's line for THIS configuration's per-update
+        # operations on it (tools/microbench, profiles/microbench_b200.json)
         mb = load_json("profiles", "microbench_b200.json") or {}
-        hot = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair")
+        bp = mb.get("bulk_pair") or {}
+        if bulk > 0 and op["repl"] > 0:
+            hot, hot_ops = bp.get("hot_k10_bulk_only_per_s_per_pair"), "one 16-B bulk reduction (reads from the SMEM replica)"
+        elif bulk > 0:
+            hot, hot_ops = bp.get("hot_k10_updates_per_s_per_pair"), "pair load + one 16-B bulk reduction"
+        elif op["split"] > 0:
+            hot, hot_ops = (mb.get("hot_line") or {}).get("ld_red_k10", {}).get("per_line"), "load + RED (x, abar split)"
+        else:
+            hot, hot_ops = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair"), "pair load + two REDs"
         out = {
             "metric": "ASAGA updates/s (one step = ingest A0-A1 + one epoch of updates A2-A8 + objective A9)",
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -322,7 +338,8 @@ def main():
             "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz,
                        "samples_in_flight": st["concurrency"], "lanes_per_sample": st["lanes_per_sample"],
                        "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale, "lambda": "10^-rank / n",
-                       "bulk_scatter_min_freq": bulk,
+                       "bulk_scatter_min_freq": bulk, "hot_split_min_freq": op["split"],
+                       "smem_replica_refresh": op["repl"],
                        "l2_flush": "512 MiB write between steps (outside the timed events)",
                        "parallelism": f"{world} independent lambda-sweep instances" if world > 1 else "1 GPU"},
             "breakdown_ms": {"ingest_A0_A1": float(np.mean(ing_ms)), "updates_A2_A8": float(np.mean(upd_ms)),
@@ -335,10 +352,10 @@ def main():
                          "kernel": "asaga_update_kernel", "bytes_per_update": bpu,
                          "peak_source": pk_kind},
             "roofline_hot_line": {
-                "bound": "L2 atomic service of the hottest feature's line (1 pair load + 2 REDs per update)",
+                "bound": f"L2 service of the hottest feature's line: {hot_ops} per update",
                 "achieved": ups, "peak": hot, "unit": "updates/s",
                 "frac": (ups / hot) if hot else None,
-                "peak_source": "tools/microbench hot_pair.k10 (profiles/microbench_b200.json)"},
+                "peak_source": "measured by tools/microbench on B200 (profiles/microbench_b200.json)"},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "f_host": f_host},
             "gpu_launches": 6 * args.steps,

@@ -518,9 +518,10 @@ def test_bench_operating_point_c2_full_size_properties():
 
     m = asaga_mod()
     p = datagen.make("c2")
-    W, gs, bulk = bench.OPERATING_POINT["c2"]
-    a = m.Asaga.from_problem(p, gs * gamma_of(p), concurrency=W, bulk_scatter_min_freq=bulk,
-                             record_samples=True)
+    op = bench.OPERATING_POINT["c2"]
+    a = m.Asaga.from_problem(p, op["gscale"] * gamma_of(p), concurrency=op["W"],
+                             bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
+                             smem_replica_refresh=op["repl"], record_samples=True)
     fs = []
     for _ in range(3):
         a.run(p.n, SEED)
