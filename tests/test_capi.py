@@ -20,8 +20,12 @@ def declared():
 
 @pytest.fixture(scope="module")
 def libpath():
-    from paper_1606_04809_b200 import _build
+    # by path: importing the package would load the library before it is built
+    import importlib.util
 
+    spec = importlib.util.spec_from_file_location("_asaga_build", os.path.join(PKG, "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)
     return _build.build()
 
 
