@@ -39,11 +39,18 @@ import datagen  # noqa: E402
 # feature frequency) from tools/sweep.py on B200 (profiles/r01_operating_point.md):
 # the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
 OPERATING_POINT = {
-    "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0),
-    "c2": dict(W=1024, gscale=0.125, bulk=0.5, split=0.0, repl=1),
-    "c3": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0),
-    "c4": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0),
+    "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
+    # c2: every feature combined per thread block (asaga_combine_kernel), 24 workers per SM
+    "c2": dict(W=3552, gscale=0.0625, bulk=0.0, split=0.0, repl=0, comb=1e-300),
+    "c3": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0, comb=0.0),
+    "c4": dict(W=256, gscale=0.35, bulk=0.0, split=0.0, repl=0, comb=0.0),
 }
+
+
+def asaga_options(op):
+    """Asaga keyword options of an operating point."""
+    return dict(bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
+                smem_replica_refresh=op["repl"], combine_min_freq=op["comb"])
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -233,9 +240,7 @@ def main():
     dev = torch.device("cuda", local)
     t = lambda arr: torch.from_numpy(arr).to(dev)
     indptr, indices, data, y = t(p.indptr), t(p.indices), t(p.data), t(p.y)
-    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local,
-              bulk_scatter_min_freq=bulk, hot_split_min_freq=op["split"],
-              smem_replica_refresh=op["repl"])
+    a = Asaga(indptr, indices, data, y, p.d, lam, 1.0, concurrency=W, device=local, **asaga_options(op))
     L = a.stats()["L"]
     gamma = gscale / (3.0 * L)
     a.set_gamma(gamma)
@@ -272,6 +277,7 @@ def main():
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    st_timed = a.stats()  # of the last timed step's update launch (combine_passes)
     step_ms = [e[0].elapsed_time(e[3]) for e in all_evs]
     upd_ms = [e[1].elapsed_time(e[2]) for e in all_evs]
     ing_ms = [e[0].elapsed_time(e[1]) for e in all_evs]
@@ -321,14 +327,23 @@ def main():
         # operations on it (tools/microbench, profiles/microbench_b200.json)
         mb = load_json("profiles", "microbench_b200.json") or {}
         bp = mb.get("bulk_pair") or {}
-        if bulk > 0 and op["repl"] > 0:
-            hot, hot_ops = bp.get("hot_k10_bulk_only_per_s_per_pair"), "one 16-B bulk reduction (reads from the SMEM replica)"
+        hot_achieved = ups
+        if op["comb"] > 0 and st_timed["combine_passes"] > 0:
+            # combining: the hot line takes one pair load + two REDs per block per pass,
+            # not per update; achieved = those line operations per second
+            hot = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair")
+            hot_ops = (f"one pair load + two REDs per thread block per communication pass "
+                       f"({st_timed['combine_passes'] / p.n:.4f} per update, {st_timed['combine_blocks']} blocks, "
+                       f"pass {upd_ms[-1] * 1e3 * st_timed['combine_blocks'] / st_timed['combine_passes']:.2f} us)")
+            hot_achieved = st_timed["combine_passes"] / (upd_ms[-1] / 1e3)
+        elif bulk > 0 and op["repl"] > 0:
+            hot, hot_ops = bp.get("hot_k10_bulk_only_per_s_per_pair"), "one 16-B bulk reduction (reads from the SMEM replica) per update"
         elif bulk > 0:
-            hot, hot_ops = bp.get("hot_k10_updates_per_s_per_pair"), "pair load + one 16-B bulk reduction"
+            hot, hot_ops = bp.get("hot_k10_updates_per_s_per_pair"), "pair load + one 16-B bulk reduction per update"
         elif op["split"] > 0:
-            hot, hot_ops = (mb.get("hot_line") or {}).get("ld_red_k10", {}).get("per_line"), "load + RED (x, abar split)"
+            hot, hot_ops = (mb.get("hot_line") or {}).get("ld_red_k10", {}).get("per_line"), "load + RED (x, abar split) per update"
         else:
-            hot, hot_ops = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair"), "pair load + two REDs"
+            hot, hot_ops = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair"), "pair load + two REDs per update"
         out = {
             "metric": "ASAGA updates/s (one step = ingest A0-A1 + one epoch of updates A2-A8 + objective A9)",
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
@@ -339,7 +354,8 @@ def main():
                        "samples_in_flight": st["concurrency"], "lanes_per_sample": st["lanes_per_sample"],
                        "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale, "lambda": "10^-rank / n",
                        "bulk_scatter_min_freq": bulk, "hot_split_min_freq": op["split"],
-                       "smem_replica_refresh": op["repl"],
+                       "smem_replica_refresh": op["repl"], "combine_min_freq": op["comb"],
+                       "combine_hot_features": st["combine_hot"],
                        "l2_flush": "512 MiB write between steps (outside the timed events)",
                        "parallelism": f"{world} independent lambda-sweep instances" if world > 1 else "1 GPU"},
             "breakdown_ms": {"ingest_A0_A1": float(np.mean(ing_ms)), "updates_A2_A8": float(np.mean(upd_ms)),
@@ -349,12 +365,13 @@ def main():
             "f_after_step": f_final,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                         "kernel": "asaga_update_kernel", "bytes_per_update": bpu,
+                         "kernel": "asaga_combine_kernel" if op["comb"] > 0 else "asaga_update_kernel",
+                         "bytes_per_update": bpu,
                          "peak_source": pk_kind},
             "roofline_hot_line": {
-                "bound": f"L2 service of the hottest feature's line: {hot_ops} per update",
-                "achieved": ups, "peak": hot, "unit": "updates/s",
-                "frac": (ups / hot) if hot else None,
+                "bound": f"L2 service of the hottest feature's line: {hot_ops}",
+                "achieved": hot_achieved, "peak": hot, "unit": "hot-line operation sets/s",
+                "frac": (hot_achieved / hot) if hot else None,
                 "peak_source": "measured by tools/microbench on B200 (profiles/microbench_b200.json)"},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "f_host": f_host},

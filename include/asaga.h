@@ -116,6 +116,22 @@ typedef struct {
                             entries from L2 every r samples.  Reads become older but stay
                             bounded-delay inconsistent reads (Assumption 1).
                             0 (default) = off. */
+  double combine_min_freq;  /* f > 0, async mode: features present in at least this fraction
+                            of rows (p_v >= f; at most 4096 of them, else ASAGA_E_INVALID_ARG at
+                            ingest) are combined per thread block: workers read a shared-memory
+                            replica of {x_v, abar_v} and add into a block-local pending pair;
+                            one warp per block sends the pending adds to the shared state
+                            (red.global.add.f64) and refreshes the replica, continuously.  The
+                            shared state then takes one add per hot feature per block per pass
+                            instead of one per sample.  Reads stay bounded-delay inconsistent
+                            reads (Assumption 1; reading R23); every
+                            add reaches the shared state before asaga_run returns.  Exclusive with
+                            the bulk scatter, hot split and replica options.  0 (default) = off;
+                            1e-300 = every used feature (small d). */
+  int combine_cluster;   /* combining: thread blocks per cluster (1..8; 0 = 8).  The blocks of
+                            a cluster share one communication pass over distributed shared
+                            memory, so the shared state takes one add per hot feature per
+                            CLUSTER per pass. */
 } asaga_options;
 
 typedef struct {
@@ -137,6 +153,11 @@ typedef struct {
   int algorithm;          /* asaga_algorithm */
   double hot_split_min_freq;
   int smem_replica;       /* 1 when the shared-memory replica is in use */
+  int combine_hot;        /* number of features combined per block (0 = combining off) */
+  int combine_blocks;     /* thread blocks (replicas) of the combine kernel */
+  int64_t combine_passes; /* communication-warp passes, summed over blocks, of the last run
+                             (pass period = last_run_ms * combine_blocks / combine_passes) */
+  int combine_cluster;    /* blocks per cluster of the combine kernel */
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

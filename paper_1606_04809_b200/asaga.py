@@ -45,7 +45,8 @@ class Options(ctypes.Structure):
                 ("atomic_mode", ctypes.c_int), ("record_samples", ctypes.c_int),
                 ("stream", ctypes.c_void_p), ("bulk_scatter_min_freq", ctypes.c_double),
                 ("measure_overlap", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double),
-                ("smem_replica_refresh", ctypes.c_int)]
+                ("smem_replica_refresh", ctypes.c_int), ("combine_min_freq", ctypes.c_double),
+                ("combine_cluster", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +59,9 @@ class Stats(ctypes.Structure):
                 ("bulk_scatter_min_freq", ctypes.c_double), ("overlap_mean", ctypes.c_double),
                 ("overlap_max", ctypes.c_int64), ("overlap_samples", ctypes.c_int64),
                 ("algorithm", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double),
-                ("smem_replica", ctypes.c_int)]
+                ("smem_replica", ctypes.c_int), ("combine_hot", ctypes.c_int),
+                ("combine_blocks", ctypes.c_int), ("combine_passes", ctypes.c_int64),
+                ("combine_cluster", ctypes.c_int)]
 
 
 ABI_FUNCTIONS = {
@@ -164,7 +167,8 @@ class Asaga:
                  deterministic: bool = False, concurrency: int = 0, lanes_per_sample: int = 0,
                  atomic: bool = True, record_samples: bool = False, device: int = 0,
                  stream=None, bulk_scatter_min_freq: float = 0.0, measure_overlap: int = 0,
-                 hot_split_min_freq: float = 0.0, smem_replica_refresh: int = 0):
+                 hot_split_min_freq: float = 0.0, smem_replica_refresh: int = 0,
+                 combine_min_freq: float = 0.0, combine_cluster: int = 0):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -186,6 +190,8 @@ class Asaga:
         opt.measure_overlap = int(measure_overlap)
         opt.hot_split_min_freq = float(hot_split_min_freq)
         opt.smem_replica_refresh = int(smem_replica_refresh)
+        opt.combine_min_freq = float(combine_min_freq)
+        opt.combine_cluster = int(combine_cluster)
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

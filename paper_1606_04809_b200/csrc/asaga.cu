@@ -56,6 +56,18 @@ struct asaga_ctx {
   double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
   double hot_dmax = 0.0;   // hot split threshold on D_c (abar in habar)
   int replica_every = 0;   // > 0: shared-memory replica of {x, abar} (small d, async)
+  double comb_freq = 0.0;  // > 0: CTA-level combining of features with p_v >= comb_freq
+  int comb_H = 0;          // ... the number of such (hot) features after ingest
+  int32_t* slot_of = nullptr;  // d: slot of a hot feature, -1 if cold
+  int32_t* hot_id = nullptr;   // kCombMaxH: slot -> feature
+  int32_t* eslot = nullptr;    // nnz: slot_of[cols[k]] (allocated when 0 < comb_H < d)
+  int comb_nwb = 0;            // worker groups per block of the combine kernel
+  int comb_csize = 1;          // blocks per cluster of the combine kernel
+  int comb_cluster_opt = 0;    // requested cluster size (0 = 8)
+  int32_t* comb_flag = nullptr;  // d scratch: hot flags, then their exclusive scan
+  int32_t* comb_excl = nullptr;
+  void* cub_temp = nullptr;
+  size_t cub_temp_bytes = 0;
   double* habar = nullptr; // abar of hot-split features
   double* D = nullptr;     // reweighting n / n_v
   double* dv = nullptr;    // D_{c_k} per stored entry
@@ -199,6 +211,100 @@ UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
 }
 
 constexpr int64_t kReplicaMaxD = 4096;  // 64 KiB of {x, abar} pairs per block
+constexpr int kCombMaxH = 4096;         // hot features combined per block: 128 KiB of xr + pend
+constexpr int kCombBlock = 512;         // max threads of a combine block (launch bounds)
+
+bool use_combine(const asaga_ctx* ctx) {
+  return ctx->comb_freq > 0.0 && !ctx->deterministic && ctx->atomic_mode && ctx->comb_H > 0;
+}
+
+template <int G, int NR>
+UpdFn pick_comb(bool full) {
+  return full ? asaga_combine_kernel<G, NR, true> : asaga_combine_kernel<G, NR, false>;
+}
+
+template <int G>
+UpdFn pick_comb_nr(int nr, bool full) {
+  switch (nr) {
+    case 1: return pick_comb<G, 1>(full);
+    case 2: return pick_comb<G, 2>(full);
+    case 4: return pick_comb<G, 4>(full);
+    default: return pick_comb<G, 8>(full);
+  }
+}
+
+UpdFn combine_fn(const asaga_ctx* ctx, int lanes, int nr) {
+  const bool full = ctx->comb_H == ctx->d;
+  switch (lanes) {
+    case 8: return pick_comb_nr<8>(nr, full);
+    case 16: return pick_comb_nr<16>(nr, full);
+    default: return pick_comb_nr<32>(nr, full);
+  }
+}
+
+size_t comb_group_bytes(const asaga_ctx* ctx) {  // CombSmem<G, NR, FULL>::bytes
+  const bool full = ctx->comb_H == ctx->d;
+  const size_t P = (size_t)ctx->nr * ctx->lanes;
+  const size_t alpha_off = P * (2 * sizeof(double) + sizeof(int32_t) + (full ? 0 : sizeof(int32_t)));
+  const size_t stage = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
+  // KS = 3 row stages + a bounds ring of 2 KS 32-byte slots + overflow q slots
+  return (3 * stage + 6 * 32 + (size_t)ctx->overflow * sizeof(double) + 15) & ~(size_t)15;
+}
+
+size_t comb_smem(const asaga_ctx* ctx, int nwb) {
+  return (size_t)ctx->comb_H * 2 * 16 + (size_t)nwb * comb_group_bytes(ctx);
+}
+
+// Combine launch shape: blocks in clusters of C (C blocks share one set of hot-feature
+// adds per pass, DSMEM); at most one block per SM and only as many clusters as can be
+// resident at once (every block runs for the whole launch).  nwb = worker groups per block.
+asaga_status comb_shape(asaga_ctx* ctx, int64_t workers, int* nwb, int* blocks, int* csize,
+                        int64_t* workers_out) {
+  const int per_warp = 32 / ctx->lanes;
+  int C = ctx->comb_cluster_opt > 0 ? ctx->comb_cluster_opt : 1;
+  C = std::max(1, std::min(C, 8));
+  int64_t groups_needed = workers;
+  // resident clusters of C blocks (1 block per SM: launch bounds + large shared memory)
+  UpdFn fn = combine_fn(ctx, ctx->lanes, ctx->nr);
+  int cap_clusters = 0;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(C * ctx->sms);
+    cfg.blockDim = dim3(kCombBlock);
+    cfg.dynamicSmemBytes = 200 * 1024;  // forces one block per SM
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(ctx, cudaOccupancyMaxActiveClusters(&cap_clusters, (const void*)fn, &cfg));
+  }
+  if (cap_clusters < 1) return fail(ctx, ASAGA_E_INVALID_ARG, "no cluster of %d blocks fits the device", C);
+  int64_t cap_blocks = (int64_t)cap_clusters * C;
+  if (workers <= 0)  // auto: every resident block full of workers
+    workers = cap_blocks * ((kCombBlock - 32) / ctx->lanes);
+  // blocks: enough that every block has <= kCombBlock - 32 worker threads
+  groups_needed = workers;
+  int64_t b = std::min<int64_t>((groups_needed + per_warp - 1) / per_warp, cap_blocks);
+  b = std::max<int64_t>(b, 1);
+  int64_t w = (groups_needed + b - 1) / b;
+  w = (w + per_warp - 1) / per_warp * per_warp;
+  if (w * ctx->lanes > kCombBlock - 32)
+    return fail(ctx, ASAGA_E_INVALID_ARG, "combine: %lld samples in flight need %lld worker threads per block "
+                "(max %d with %lld resident blocks)", (long long)workers, (long long)(w * ctx->lanes),
+                kCombBlock - 32, (long long)cap_blocks);
+  b = (groups_needed + w - 1) / w;
+  const int Ce = (int)std::min<int64_t>(C, b);
+  b = (b + Ce - 1) / Ce * Ce;
+  *nwb = (int)w;
+  *blocks = (int)b;
+  *csize = Ce;
+  *workers_out = workers;
+  return ASAGA_OK;
+}
 
 bool use_replica(const asaga_ctx* ctx) {
   return ctx->replica_every > 0 && !ctx->deterministic && ctx->d <= kReplicaMaxD;
@@ -248,6 +354,31 @@ asaga_status configure_update(asaga_ctx* ctx) {
                              2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
                              (size_t)ctx->overflow * sizeof(double);
   ctx->group_bytes = group_bytes;
+  if (use_combine(ctx)) {
+    int64_t workers = ctx->concurrency_opt > 0 ? ctx->concurrency_opt : 0;
+    int nwb = 1, blocks = 1, csize = 1;
+    TRY(comb_shape(ctx, workers, &nwb, &blocks, &csize, &workers));
+    if (ctx->concurrency_opt <= 0)  // auto: as many workers as the shared memory allows
+      while (nwb > 32 / lanes && comb_smem(ctx, nwb) > 226 * 1024) {
+        workers = (int64_t)blocks * (nwb - 32 / lanes);
+        TRY(comb_shape(ctx, workers, &nwb, &blocks, &csize, &workers));
+      }
+    ctx->smem = comb_smem(ctx, nwb);
+    if (ctx->smem > 226 * 1024)
+      return fail(ctx, ASAGA_E_INVALID_ARG,
+                  "combine: %d hot features and %d workers per block need %zu B of shared memory "
+                  "(raise combine_min_freq or lower the concurrency)", ctx->comb_H, nwb, ctx->smem);
+    UpdFn cfn = combine_fn(ctx, lanes, nr);
+    CK(ctx, cudaFuncSetAttribute((const void*)cfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)ctx->smem));
+    ctx->comb_nwb = nwb;
+    ctx->comb_csize = csize;
+    ctx->workers = workers;
+    ctx->block = nwb * lanes + 32;
+    ctx->grid = blocks;
+    ctx->max_resident_groups = (int)std::min<int64_t>(INT32_MAX, workers);
+    return ASAGA_OK;
+  }
   ctx->smem = replica_bytes(ctx) + (size_t)groups_per_block * group_bytes;
   UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 227 * 1024)
@@ -291,13 +422,25 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->tmp_n, n));
   TRY(dalloc(ctx, &ctx->tmp_d, d));
   TRY(dalloc(ctx, &ctx->tmp_d2, d));
-  ctx->obj_blocks = ctx->sms * 6;  // 48 resident warps per SM at 40 registers (fixed: deterministic sums)
+  ctx->obj_blocks = ctx->sms * 5;  // 40 resident warps per SM at 48 registers (fixed: deterministic sums)
   TRY(dalloc(ctx, &ctx->block_loss, ctx->obj_blocks));
   TRY(dalloc(ctx, &ctx->scal, 4));
   TRY(dalloc(ctx, &ctx->flag, 4));
-  TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 2));  // err rows, max ||a||^2, max row
+  TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
+  if (ctx->comb_freq > 0.0) {
+    TRY(dalloc(ctx, &ctx->slot_of, d));
+    TRY(dalloc(ctx, &ctx->hot_id, kCombMaxH));
+    TRY(dalloc(ctx, &ctx->comb_flag, d));
+    TRY(dalloc(ctx, &ctx->comb_excl, d));
+    TRY(dalloc(ctx, &ctx->eslot, nnz));  // written only when some features stay cold
+    CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, ctx->cub_temp_bytes, ctx->comb_flag, ctx->comb_excl,
+                                          (int)d, ctx->stream));
+    unsigned char* tb = nullptr;
+    TRY(dalloc(ctx, &tb, ctx->cub_temp_bytes));
+    ctx->cub_temp = tb;
+  }
   return ASAGA_OK;
 }
 
@@ -348,29 +491,36 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
   const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 0;
-  const double mean = n ? (double)nnz / (double)n : 1.0;
-  const void* kfn = mean <= 8.0 ? (const void*)ingest_kernel<8>
-                    : mean <= 16.0 ? (const void*)ingest_kernel<16> : (const void*)ingest_kernel<32>;
-  const int gl = mean <= 8.0 ? 8 : (mean <= 16.0 ? 16 : 32);
-  constexpr int kIngestBlock = 1024;
+  const void* kfn = (const void*)ingest_tile_kernel;
+  constexpr int kIngestBlock = 256;
   CK(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
   int per_sm = 1;
   CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kIngestBlock, hsmem));
   per_sm = std::max(per_sm, 1);
-  const int64_t want = (n + (kIngestBlock / gl) - 1) / (kIngestBlock / gl);
+  const int64_t want = (n + 32 * (kIngestBlock / 32) - 1) / (32 * (kIngestBlock / 32));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
   void* iargs[] = {&ip};
   CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
   profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, d, n,
                                                                         ctx->flag + 1);
   CK(ctx, cudaGetLastError());
-  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(ctx->cols, ctx->D, nnz,
-                                                                          ctx->hot_dmax, ctx->dv);
+  if (ctx->comb_freq > 0.0) {  // hot set of the combine kernel: p_v >= combine_min_freq
+    hot_flag_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->D, d, 1.0 / ctx->comb_freq,
+                                                                          ctx->comb_flag);
+    CK(ctx, cudaGetLastError());
+    CK(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp, ctx->cub_temp_bytes, ctx->comb_flag, ctx->comb_excl,
+                                          (int)d, ctx->stream));
+    hot_slot_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(
+        ctx->comb_flag, ctx->comb_excl, d, kCombMaxH, ctx->slot_of, ctx->hot_id, ctx->flag + 2);
+    CK(ctx, cudaGetLastError());
+  }
+  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(
+      ctx->cols, ctx->D, nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, d, ctx->eslot);
   CK(ctx, cudaGetLastError());
   unsigned long long h[ERR_COUNT + 2];
-  int hmax_count = 0;
+  int hflag[2] = {0, 0};  // max_v n_v, number of hot features
   CK(ctx, cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(ctx, cudaMemcpyAsync(&hmax_count, ctx->flag + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(hflag, ctx->flag + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
   CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
   static const char* what[ERR_COUNT] = {"row pointers out of order or out of [0, nnz]",
@@ -389,7 +539,17 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   std::memcpy(&max_sq, &h[ERR_COUNT], sizeof(double));
   ctx->L = max_sq / 4.0 + ctx->lambda;
   ctx->max_row = (int64_t)h[ERR_COUNT + 1];
-  ctx->delta_r = hmax_count;
+  ctx->delta_r = hflag[0];
+  if (ctx->comb_freq > 0.0) {
+    if (hflag[1] > kCombMaxH && hflag[1] < d)
+      return fail(ctx, ASAGA_E_INVALID_ARG,
+                  "combine_min_freq=%g selects %d features; at most %d fit a block (raise it)",
+                  ctx->comb_freq, hflag[1], kCombMaxH);
+    ctx->comb_H = hflag[1];
+    if (ctx->comb_H == d && d > kCombMaxH)
+      return fail(ctx, ASAGA_E_INVALID_ARG, "combine_min_freq=%g selects all %lld features; at most %d fit",
+                  ctx->comb_freq, (long long)d, kCombMaxH);
+  }
   return configure_update(ctx);
 }
 
@@ -439,6 +599,20 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   }
   ctx->hot_dmax = o.hot_split_min_freq > 0.0 ? 1.0 / o.hot_split_min_freq : 0.0;
   ctx->replica_every = o.smem_replica_refresh > 0 ? o.smem_replica_refresh : 0;
+  if (!(o.combine_min_freq >= 0.0) || o.combine_min_freq > 1.0 ||
+      (o.combine_min_freq > 0.0 && (o.hot_split_min_freq > 0.0 || o.bulk_scatter_min_freq > 0.0 ||
+                                    o.smem_replica_refresh > 0))) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG,
+                "combine_min_freq must be in [0, 1] and cannot be combined with the bulk scatter, "
+                "the hot split or the replica");
+  }
+  ctx->comb_freq = o.combine_min_freq;
+  if (o.combine_cluster < 0 || o.combine_cluster > 8) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG, "combine_cluster must be in [0, 8] (got %d)", o.combine_cluster);
+  }
+  ctx->comb_cluster_opt = o.combine_cluster;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
   if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
@@ -549,17 +723,9 @@ asaga_status ensure_csc(asaga_ctx* ctx) {
 // (element stride xs: 1 for a dense vector, 2 for the {x, abar} pairs).
 asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, double* f_dev,
                                double* loss_sum_dev, bool want_sig, cudaStream_t s) {
-  const double mean = (double)ctx->nnz / (double)ctx->n;
   double* sig = want_sig ? ctx->sig : nullptr;
-  if (mean <= 8.0)
-    margin_kernel<8><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                        ctx->n, sig, ctx->block_loss);
-  else if (mean <= 16.0)
-    margin_kernel<16><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                         ctx->n, sig, ctx->block_loss);
-  else
-    margin_kernel<32><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                         ctx->n, sig, ctx->block_loss);
+  margin_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs, ctx->n, sig,
+                                                   ctx->block_loss);
   CK(ctx, cudaGetLastError());
   finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, xs, ctx->d,
                                              ctx->n, ctx->lambda, f_dev, loss_sum_dev);
@@ -615,6 +781,36 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
 #ifdef ASAGA_TIMING
   if (const char* m = getenv("ASAGA_DEBUG_MODE")) p.debug_mode = atoi(m);
 #endif
+  p.H = ctx->comb_H;
+  p.nwb = ctx->comb_nwb;
+  p.hot_id = ctx->hot_id;
+  p.eslot = ctx->eslot;
+  p.comm_passes = ctx->comb_freq > 0.0 ? ctx->scratch + ERR_COUNT + 2 : nullptr;
+  if (p.comm_passes && use_combine(ctx))
+    CK(ctx, cudaMemsetAsync(p.comm_passes, 0, sizeof(unsigned long long), ctx->stream));
+  if (use_combine(ctx)) {
+    const int64_t need = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
+    int grid = (int)((need + ctx->comb_nwb - 1) / ctx->comb_nwb);
+    grid = (grid + ctx->comb_csize - 1) / ctx->comb_csize * ctx->comb_csize;
+    UpdFn cfn = combine_fn(ctx, ctx->lanes, ctx->nr);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ctx->comb_csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(ctx->block);
+    cfg.dynamicSmemBytes = ctx->smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
+    CK(ctx, cudaLaunchKernelEx(&cfg, cfn, p));
+    if (timed) CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
+    ctx->t += n_updates;
+    return ASAGA_OK;
+  }
   UpdFn fn = update_fn(ctx, ctx->lanes, ctx->nr);
   // Fewer updates than workers: launch only what is needed.  The stride stays W,
   // so the t -> worker map does not depend on the launch.
@@ -648,6 +844,8 @@ void asaga_options_default(asaga_options* opt) {
   opt->bulk_scatter_min_freq = 0.0;
   opt->hot_split_min_freq = 0.0;
   opt->smem_replica_refresh = 0;
+  opt->combine_min_freq = 0.0;
+  opt->combine_cluster = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -894,6 +1092,15 @@ asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
   out->algorithm = ctx->algorithm;
   out->hot_split_min_freq = ctx->hot_dmax > 0.0 ? 1.0 / ctx->hot_dmax : 0.0;
   out->smem_replica = use_replica(ctx) ? 1 : 0;
+  out->combine_hot = use_combine(ctx) ? ctx->comb_H : 0;
+  out->combine_blocks = use_combine(ctx) ? ctx->grid : 0;
+  out->combine_cluster = use_combine(ctx) ? ctx->comb_csize : 0;
+  out->combine_passes = 0;
+  if (use_combine(ctx)) {
+    unsigned long long c = 0;
+    if (cudaMemcpy(&c, ctx->scratch + ERR_COUNT + 2, sizeof(c), cudaMemcpyDeviceToHost) == cudaSuccess)
+      out->combine_passes = (int64_t)c;
+  }
   out->overlap_mean = 0.0;
   out->overlap_max = 0;
   out->overlap_samples = 0;

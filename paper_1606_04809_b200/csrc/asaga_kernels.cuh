@@ -131,7 +131,7 @@ struct IngestParams {
 // and the longest row.  Rows go to G-lane groups; each element is read once (the
 // previous index for the order check comes from a shuffle).
 template <int G>
-__global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
+__global__ void __launch_bounds__(512) ingest_kernel(IngestParams p) {
   extern __shared__ int32_t hist[];
   __shared__ double blk_max[32];
   __shared__ long long blk_len[32];
@@ -145,8 +145,33 @@ __global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
   double my_max = 0.0;
   long long my_len = 0;
   const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; i < p.n; i += groups) {
-    const int64_t lo = p.indptr[i], hi = p.indptr[i + 1];
+  // U rows per group in flight: their bounds, labels and first chunk are loaded before
+  // any of them is processed (one row at a time left the pass latency-bound)
+  constexpr int U = 4;
+  for (int64_t i0 = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; i0 < p.n; i0 += U * groups) {
+    int64_t lo_u[U], hi_u[U];
+    double b_u[U];
+    int32_t c_u[U];
+    double v_u[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * groups;
+      lo_u[u] = i < p.n ? p.indptr[i] : 0;
+      hi_u[u] = i < p.n ? p.indptr[i + 1] : 0;
+      b_u[u] = i < p.n ? p.y[i] : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = lo_u[u] + g;
+      const bool ok = lo_u[u] >= 0 && hi_u[u] <= p.nnz && k < hi_u[u];
+      c_u[u] = ok ? p.indices[k] : INT32_MAX;
+      v_u[u] = ok ? p.data[k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + u * groups;
+    if (i >= p.n) break;  // group-uniform
+    const int64_t lo = lo_u[u], hi = hi_u[u];
     if (g == 0) {
       p.rowptr_out[i] = lo;
       if (i == p.n - 1) p.rowptr_out[p.n] = hi;
@@ -160,7 +185,7 @@ __global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
       continue;
     }
     my_len = max(my_len, (long long)(hi - lo));
-    const double b = p.y[i];
+    const double b = b_u[u];
     if (g == 0) {
       p.y_out[i] = b;
       if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
@@ -171,8 +196,8 @@ __global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
     for (int64_t base = lo; base < hi; base += G) {
       const int64_t k = base + g;
       const bool in = k < hi;
-      const int32_t c = in ? p.indices[k] : INT32_MAX;
-      const double v = in ? p.data[k] : 0.0;
+      const int32_t c = base == lo ? c_u[u] : (in ? p.indices[k] : INT32_MAX);
+      const double v = base == lo ? v_u[u] : (in ? p.data[k] : 0.0);
       int prev = __shfl_up_sync(gmask, c, 1, G);
       if (g == 0) prev = carry;
       if (in) {
@@ -197,8 +222,151 @@ __global__ void __launch_bounds__(1024) ingest_kernel(IngestParams p) {
       atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
     sq = group_sum<G>(sq, gmask);
     my_max = fmax(my_max, sq);
+    }
   }
   // block maxima (warp shuffles, then one atomic per block)
+  for (int off = 16; off > 0; off >>= 1) {
+    my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
+    my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
+  }
+  if (lane == 0) {
+    blk_max[wib] = my_max;
+    blk_len[wib] = my_len;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    long long L = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      m = fmax(m, blk_max[w]);
+      L = max(L, blk_len[w]);
+    }
+    atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
+    atomicMax(p.max_len, (unsigned long long)L);
+  }
+  if (p.smem_hist) {
+    __syncthreads();
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
+      if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row tiles (A0+A1 ingest, A9 margins).  A warp owns 32 consecutive rows and streams
+// their entries [rowptr[r0], rowptr[r0+32]) flat, 32 per chunk (coalesced loads, many
+// chunks in flight), instead of one row per lane group (three dependent round trips
+// per row: the per-row kernels were latency-bound at 0.8-1 TB/s).  Lane j holds the
+// tile-relative start of row r0+j; an entry finds its row by a 5-step binary search
+// over the lanes, and per-row sums use a segmented warp reduction whose segment heads
+// add into the warp's shared row accumulators (fixed order: deterministic).
+__device__ __forceinline__ int tile_row_of(int off, int rel, int nr) {
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const int cand = j + step;
+    const int rc = __shfl_sync(0xffffffffu, rel, cand & 31);
+    if (cand < nr && rc <= off) j = cand;
+  }
+  return j;
+}
+// Segmented sum over lanes with equal keys (keys non-decreasing across lanes): the
+// first lane of each segment receives the segment's total.
+__device__ __forceinline__ double seg_sum_head(double v, int key, bool* head) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double ov = __shfl_down_sync(0xffffffffu, v, d);
+    const int ok = __shfl_down_sync(0xffffffffu, key, d);
+    if (lane + d < 32 && ok == key) v += ov;
+  }
+  const int pk = __shfl_up_sync(0xffffffffu, key, 1);
+  *head = lane == 0 || pk != key;
+  return v;
+}
+
+// A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
+// values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
+__global__ void __launch_bounds__(256) ingest_tile_kernel(IngestParams p) {
+  extern __shared__ int32_t hist[];
+  __shared__ double rsq[8][32];
+  __shared__ double blk_max[8];
+  __shared__ long long blk_len[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (p.smem_hist) {
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
+    __syncthreads();
+  }
+  double my_max = 0.0;
+  long long my_len = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * 32 < p.n; tile += nwarps) {
+    const int64_t r0 = tile * 32;
+    const int nr = (int)((p.n - r0) < 32 ? (p.n - r0) : 32);
+    const int64_t i = r0 + lane;
+    const bool row = lane < nr;
+    const int64_t lo = row ? p.indptr[i] : 0;
+    const int64_t hi = row ? p.indptr[i + 1] : 0;
+    const double b = row ? p.y[i] : 1.0;
+    if (row) {
+      p.rowptr_out[i] = lo;
+      if (i == p.n - 1) p.rowptr_out[p.n] = hi;
+      p.y_out[i] = b;
+      if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
+    }
+    // bounds: every row inside [0, nnz], monotone, contiguous with the next row
+    const int64_t next_lo = __shfl_down_sync(0xffffffffu, lo, 1);
+    const bool bad_b = row && (lo < 0 || hi > p.nnz || hi < lo || (lane + 1 < nr && next_lo != hi));
+    if (bad_b) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
+    if (__any_sync(0xffffffffu, bad_b)) continue;  // the tile cannot be streamed
+    if (row && hi == lo) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
+    if (row) my_len = max(my_len, (long long)(hi - lo));
+    const int64_t base = __shfl_sync(0xffffffffu, lo, 0);
+    const int64_t end = __shfl_sync(0xffffffffu, hi, nr - 1);
+    const int rel = (int)((row ? lo : end) - base);
+    rsq[wib][lane] = 0.0;
+    __syncwarp();
+    int carry = -1;
+    bool bad_range = false, bad_order = false, bad_val = false;
+    int first_bad_range = INT32_MAX, first_bad_order = INT32_MAX, first_bad_val = INT32_MAX;
+#pragma unroll 2
+    for (int64_t e0 = base; e0 < end; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool in = e < end;
+      const int32_t c = in ? p.indices[e] : INT32_MAX;
+      const double v = in ? p.data[e] : 0.0;
+      const int off = (int)(e - base);
+      const int j = tile_row_of(off, rel, nr);
+      const int rs = __shfl_sync(0xffffffffu, rel, j);
+      const double bj = __shfl_sync(0xffffffffu, b, j);
+      int prev = __shfl_up_sync(0xffffffffu, c, 1);
+      if (lane == 0) prev = carry;
+      carry = __shfl_sync(0xffffffffu, c, 31);
+      if (in) {
+        const bool br = (c < 0) || ((int64_t)c >= p.d);
+        const bool bo = off > rs && prev >= c;
+        const bool bv = !isfinite(v);
+        if (br) first_bad_range = min(first_bad_range, j);
+        if (bo) first_bad_order = min(first_bad_order, j);
+        if (bv) first_bad_val = min(first_bad_val, j);
+        bad_range |= br; bad_order |= bo; bad_val |= bv;
+        p.cols_out[e] = c;
+        p.vals[e] = bj * v;
+        if (!br) {
+          if (p.smem_hist) atomicAdd(&hist[c], 1);
+          else atomicAdd(&p.counts[c], 1);
+        }
+      }
+      bool head;
+      const double sq = seg_sum_head(in ? v * v : 0.0, in ? j : 32 + lane, &head);
+      if (in && head) rsq[wib][j] += sq;
+    }
+    if (bad_range) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)(r0 + first_bad_range));
+    if (bad_order) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)(r0 + first_bad_order));
+    if (bad_val) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)(r0 + first_bad_val));
+    __syncwarp();
+    if (row) my_max = fmax(my_max, rsq[wib][lane]);
+    __syncwarp();
+  }
   for (int off = 16; off > 0; off >>= 1) {
     my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
     my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
@@ -246,12 +414,42 @@ __global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __re
 // Hot split (hot_dmax > 0): an entry of a popular feature (D_c <= hot_dmax, i.e.
 // p_c >= 1/hot_dmax) carries -D_c: its abar lives in the separate `habar` array, so
 // x_c and abar_c sit on different L2 lines (2 operations per line per update, not 3).
+// Combining (asaga_combine_kernel): eslot[k] = slot of the entry's feature (-1 cold),
+// written only when some but not all features are hot (*n_hot < d).
 __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* __restrict__ D,
-                                int64_t nnz, double hot_dmax, double* __restrict__ dv) {
+                                int64_t nnz, double hot_dmax, double* __restrict__ dv,
+                                const int32_t* __restrict__ slot_of, const int* __restrict__ n_hot,
+                                int64_t d, int32_t* __restrict__ eslot) {
+  const bool want_slot = eslot != nullptr && *n_hot > 0 && (int64_t)*n_hot < d;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const double Dc = __ldg(D + cols[k]);
+    const int c = cols[k];
+    const double Dc = __ldg(D + c);
     dv[k] = (hot_dmax > 0.0 && Dc <= hot_dmax) ? -Dc : Dc;
+    if (want_slot) eslot[k] = __ldg(slot_of + c);
+  }
+}
+
+// Combining: hot features are those with 0 < D_v <= comb_dmax (p_v >= combine_min_freq).
+__global__ void hot_flag_kernel(const double* __restrict__ D, int64_t d, double comb_dmax,
+                                int32_t* __restrict__ flag) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x)
+    flag[v] = (D[v] > 0.0 && D[v] <= comb_dmax) ? 1 : 0;
+}
+
+// slot of a hot feature = number of hot features before it (exclusive scan `excl`);
+// slot_of[v] = -1 for cold ones and for slots beyond max_h; n_hot = the total.
+__global__ void hot_slot_kernel(const int32_t* __restrict__ flag, const int32_t* __restrict__ excl,
+                                int64_t d, int max_h, int32_t* __restrict__ slot_of,
+                                int32_t* __restrict__ hot_id, int* __restrict__ n_hot) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int s = excl[v];
+    const bool hot = flag[v] != 0;
+    slot_of[v] = (hot && s < max_h) ? s : -1;
+    if (hot && s < max_h) hot_id[s] = (int32_t)v;
+    if (v == d - 1) *n_hot = s + (hot ? 1 : 0);
   }
 }
 
@@ -303,6 +501,12 @@ struct UpdateParams {
   double bulk_dmax;     // MODE 2: entries with D_c <= bulk_dmax (popular features,
                         // p_c >= 1/bulk_dmax) use the TMA bulk pair reduction, others REDs
   int debug_mode;       // profiling build only: bit0 skip the scatter, bit1 skip exp/div
+  // asaga_combine_kernel only
+  int H;                  // hot features combined per block (slots 0..H-1)
+  int nwb;                // worker groups per block
+  const int32_t* hot_id;  // slot -> feature (NULL when every feature is hot: slot = feature)
+  const int32_t* eslot;   // per stored entry: slot of its feature, or -1 (cold)
+  unsigned long long* comm_passes;  // += communication-warp passes (asaga_stats)
 };
 
 // cp.async (LDGSTS) helpers: the next sample's row is copied global -> shared
@@ -650,37 +854,465 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// A2..A8 with CTA-level combining of the hot features (async only; option
+// combine_hot).  Every update touches the few most popular features, and L2 serves
+// one line's operations serially, so with every sample sending its adds straight to
+// L2 the hottest line caps the update rate (profiles/r01_update_kernel.md).  Here
+// each thread block keeps, for H hot features (slot s -> feature hot_id[s], or all
+// d features with slot = feature when FULL):
+//   xr[s]   a replica of {x_v, abar_v} the workers read (an LDS, no L2 round trip)
+//   pend[s] the block's adds not yet sent to L2 (shared-memory atomic adds)
+// and one communication warp loops: take pend[s] (atomic exchange with 0), send it
+// to the shared state with red.global.add.f64, re-read the shared pair and store
+// xr[s] = shared + pend[s].  The shared state therefore receives one add per hot
+// feature per block per pass instead of one per sample, and every coordinate a
+// worker reads is the shared value of a recent moment plus some of the block's own
+// recent adds: x^ = x_t minus a bounded set of recent updates -- the paper's
+// inconsistent read with a larger, still bounded, overlap (Assumption 1, P:316-322;
+// DESIGN.md reading R23).  Cold features (slot -1) are read from / added to L2 per
+// sample exactly as in asaga_update_kernel.  Every add reaches the shared state
+// (the comm warp flushes pend after the block's workers finish), so the quiescent
+// identity abar = (1/n) sum_i alpha_i a_i holds as in the plain kernel.
+// Worker w = blockIdx.x * nwb + (thread / G), processes t = t0 + w + kW as in
+// asaga_update_kernel (same t -> worker map).  The next sample's alpha_i is loaded
+// one sample early, with its row.
+template <int G, int NR, bool FULL>
+struct CombSmem {
+  static constexpr int P = NR * G;
+  static constexpr int KS = 3;  // row stages: rows are copied KS samples ahead
+  // per stage: fp64 value, fp64 D, int32 column, int32 slot (!FULL), then alpha_i
+  static constexpr size_t alpha_off = (size_t)P * (2 * sizeof(double) + sizeof(int32_t) +
+                                                   (FULL ? 0 : sizeof(int32_t)));
+  static constexpr size_t stage_bytes = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
+  // bounds ring: {lo, hi, i} of samples fetched 2 KS ahead (cp.async, no register waits)
+  static constexpr int NB = 2 * KS;
+  static constexpr size_t ring_off = KS * stage_bytes;
+  static constexpr size_t ring_bytes = NB * 32;
+  static __host__ __device__ size_t bytes(int overflow) {
+    return ((ring_off + ring_bytes + (size_t)overflow * sizeof(double)) + 15) & ~(size_t)15;
+  }
+};
+
+__device__ __forceinline__ double2 lds_vol2(const double2* p) {
+  double2 v;
+  asm volatile("ld.volatile.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+__device__ __forceinline__ double2 ld_relaxed2(const double2* p) {
+  double2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+  return v;
+}
+// Thread-block-cluster helpers (DSMEM): addresses are 32-bit shared::cluster windows.
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned mapa_shared(const void* p, unsigned rank) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a)
+               : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(rank));
+  return a;
+}
+// all (non-exited) threads of all blocks of the cluster; release / acquire
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ double exch_cluster_f64(unsigned a) {
+  unsigned long long old;
+  asm volatile("atom.shared::cluster.exch.b64 %0, [%1], %2;" : "=l"(old) : "r"(a), "l"(0ull) : "memory");
+  return __longlong_as_double((long long)old);
+}
+__device__ __forceinline__ double ld_cluster_f64(unsigned a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_cluster_v2(unsigned a, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ int ld_cluster_volatile_s32(unsigned a) {
+  int v;
+  asm volatile("ld.volatile.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void atomic_add_cluster_s32(unsigned a, int v) {
+  asm volatile("red.shared::cluster.add.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ double exch_shared(double* p) {
+  return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p), 0ull));
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int G, int NR, bool FULL>
+__device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage, const int32_t* cols,
+                                                 const int32_t* eslot, const double* vals,
+                                                 const double* dv, const double* alpha_i, int64_t lo,
+                                                 int64_t hi, int g) {
+  constexpr int P = NR * G;
+  unsigned char* sb = base + stage * CombSmem<G, NR, FULL>::stage_bytes;
+  if (g == 0) cp_async8(sb + CombSmem<G, NR, FULL>::alpha_off, alpha_i);
+  double* sv = reinterpret_cast<double*>(sb);
+  double* sd = sv + P;
+  int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
+  int32_t* ss = sc + P;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    if (lo + j * G >= hi) break;  // group-uniform
+    const int64_t k = lo + j * G + g;
+    if (k < hi) {
+      cp_async4(sc + j * G + g, cols + k);
+      if (!FULL) cp_async4(ss + j * G + g, eslot + k);
+      cp_async8(sv + j * G + g, vals + k);
+      cp_async8(sd + j * G + g, dv + k);
+    }
+  }
+  cp_async_commit();
+}
+
+template <int G, int NR, bool FULL>
+__global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int P = NR * G;
+  __shared__ int done;  // rank 0's copy counts the finished worker groups of the cluster
+  const int H = p.H;
+  double2* xr = reinterpret_cast<double2*>(smem_raw);
+  double2* pend = xr + H;
+  unsigned char* stage_base = smem_raw + (size_t)H * 2 * sizeof(double2);
+  const int nwb = p.nwb;  // worker groups in this block (nwb * G is a multiple of 32)
+  const unsigned crank = cluster_ctarank(), csize = cluster_nctarank();
+  for (int s = threadIdx.x; s < H; s += blockDim.x) {
+    const int64_t v = FULL ? s : p.hot_id[s];
+    xr[s] = ld_relaxed2(p.xa + v * p.S);
+    pend[s] = make_double2(0.0, 0.0);
+  }
+  if (threadIdx.x == 0) done = 0;
+  cluster_sync_all();  // every block's replica and counter exist before any remote access
+  const unsigned done0 = mapa_shared(&done, 0);
+
+  if ((int)threadIdx.x >= nwb * G) {
+    // ---------------- communication warp of cluster rank r: slots s = r (mod csize).
+    // Per pass, for each of its slots: take the pending pair of EVERY block of the
+    // cluster (remote atomic exchanges over DSMEM), send the sum with red.global.add.f64
+    // (one add per hot feature per cluster per pass), re-read the shared pair and store
+    // it into every block's replica.
+    const int lane = threadIdx.x & 31;
+    const int total = nwb * (int)csize;
+    constexpr int B = 4;  // slots per lane per batch (their loads in flight together)
+    unsigned long long passes = 0;
+    const volatile int* vdone = &done;
+    const bool solo = csize == 1;  // one block per cluster: plain shared-memory operations
+    while ((solo ? *vdone : ld_cluster_volatile_s32(done0)) < total) {
+      ++passes;
+      for (int s0 = (int)crank + (int)csize * lane; s0 < H; s0 += (int)csize * 32 * B) {
+        double2 gv[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int s = s0 + (int)csize * 32 * b;
+          if (s < H) {
+            const int64_t v = FULL ? s : p.hot_id[s];
+            double2* gp = p.xa + v * p.S;
+            double dx = 0.0, dy = 0.0;
+            if (solo) {
+              dx = exch_shared(&pend[s].x);
+              dy = exch_shared(&pend[s].y);
+            } else {
+              for (unsigned k = 0; k < csize; ++k) {
+                const unsigned a = mapa_shared(&pend[s], k);
+                dx += exch_cluster_f64(a);
+                dy += exch_cluster_f64(a + 8);
+              }
+            }
+            if (dx != 0.0) red_add(&gp->x, dx);
+            if (dy != 0.0) red_add(&gp->y, dy);
+            gv[b] = ld_relaxed2(gp);  // after this thread's own adds (same address)
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const int s = s0 + (int)csize * 32 * b;
+          if (s < H) {
+            if (solo) {  // + the adds that arrived since the exchange
+              const double2 q = lds_vol2(pend + s);
+              xr[s] = make_double2(gv[b].x + q.x, gv[b].y + q.y);
+            } else {
+              for (unsigned k = 0; k < csize; ++k) st_cluster_v2(mapa_shared(&xr[s], k), gv[b]);
+            }
+          }
+        }
+      }
+    }
+    cluster_sync_all();  // every worker of the cluster has finished its adds to pend
+    if (lane == 0 && p.comm_passes != nullptr) atomicAdd(p.comm_passes, passes);
+    for (int s = (int)crank + (int)csize * lane; s < H; s += (int)csize * 32) {
+      const int64_t v = FULL ? s : p.hot_id[s];
+      double2* gp = p.xa + v * p.S;
+      double dx = 0.0, dy = 0.0;
+      for (unsigned k = 0; k < csize; ++k) {
+        const unsigned a = mapa_shared(&pend[s], k);
+        dx += ld_cluster_f64(a);
+        dy += ld_cluster_f64(a + 8);
+      }
+      if (dx != 0.0) red_add(&gp->x, dx);
+      if (dy != 0.0) red_add(&gp->y, dy);
+    }
+    cluster_sync_all();  // no block exits while another may still read its pend
+    return;
+  }
+
+  // ---------------- workers
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
+  const int grp = threadIdx.x / G;
+  const int64_t w = (int64_t)blockIdx.x * nwb + grp;
+  using SM = CombSmem<G, NR, FULL>;
+  constexpr int KS = SM::KS;
+  unsigned char* gbase = stage_base + (size_t)grp * SM::bytes(p.overflow);
+  double* qs = reinterpret_cast<double*>(gbase + SM::ring_off + SM::ring_bytes);
+  int64_t* ring = reinterpret_cast<int64_t*>(gbase + SM::ring_off);  // slot k: ring[4k..4k+2]
+  const uint64_t tend = p.t0 + p.T;
+  const uint64_t W = (uint64_t)p.workers;
+  const uint64_t t_first = p.t0 + (uint64_t)w;
+  uint64_t t = t_first;
+  if (w < p.workers && t < tend) {
+    // Pipeline over this worker's samples m = 0, 1, ... (t = t_first + mW), all of it
+    // read-only data, so fetching early changes nothing but latency:
+    //   the row (+ alpha_i) of sample m + KS is copied at iteration m (KS stages),
+    //   the bounds {lo, hi} (+ i) of sample m + 2KS are copied at iteration m (ring).
+    // One cp.async group per iteration; wait_group<KS-1> at iteration m completes the
+    // group of iteration m - KS, which holds the row of m and the bounds of m + KS.
+    // (A register queue of bounds made the loop wait on the newest rowptr load.)
+    // Sample indices come in batches of G: lane j draws sample mb + j (one Philox per
+    // lane per G samples instead of one per sample), shuffled out in order.
+    int64_t bi = 0;
+    auto draw_batch = [&](uint64_t mb) {
+      const uint64_t ts = t_first + (mb + (uint64_t)g) * W;
+      bi = ts < tend ? sample_row(p.seed, ts, p.n) : 0;
+    };
+    auto sample_of = [&](uint64_t ms) -> int64_t {  // group-uniform call; batch of ms drawn
+      return __shfl_sync(gmask, bi, (int)(ms & (uint64_t)(G - 1)), G);
+    };
+    static_assert(G >= 2 * KS, "a batch covers the prologue's samples");
+    auto fetch_bounds = [&](uint64_t m, int slot_k) {
+      const uint64_t ts = t_first + m * W;
+      const int64_t is = sample_of(m);
+      if (g == 0 && ts < tend) {
+        int64_t* slot = ring + 4 * slot_k;
+        slot[2] = is;
+        cp_async8(slot, p.rowptr + is);
+        cp_async8(slot + 1, p.rowptr + is + 1);
+      }
+    };
+    draw_batch(0);
+#pragma unroll 1
+    for (int k = 0; k < KS; ++k) {  // prologue: rows of samples 0..KS-1, bounds of KS..2KS-1
+      const uint64_t ts = t_first + (uint64_t)k * W;
+      const int64_t is = sample_of((uint64_t)k);
+      fetch_bounds((uint64_t)(k + KS), k + KS);
+      if (ts < tend) {
+        const int64_t l0 = __ldg(&p.rowptr[is]), h0 = __ldg(&p.rowptr[is + 1]);
+        if (g == 0) { ring[4 * k] = l0; ring[4 * k + 1] = h0; ring[4 * k + 2] = is; }
+        issue_row_copy_c<G, NR, FULL>(gbase, k, p.cols, p.eslot, p.vals, p.dv, p.alpha + is, l0, h0, g);
+      } else {
+        cp_async_commit();
+      }
+    }
+    unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
+    int ov_local = 0, ov_iter = 0;
+    int stage = 0, rs = 0;  // row stage and bounds-ring slot of sample m
+    for (uint64_t m = 0;; ++m) {
+      const bool ov_meas = p.ov != nullptr && (ov_iter++ % p.ov_every) == 0;
+      unsigned long long ov_c0 = 0;
+      if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
+      cp_async_wait_group<KS - 1>();  // this sample's stage (and bounds of m + KS) landed
+      __syncwarp(gmask);             // lane 0 copied alpha_i and the bounds
+      const int64_t* cur = ring + 4 * rs;
+      const int64_t lo = cur[0], hi = cur[1], i = cur[2];
+      const double* sv = reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes);
+      const double* sd = sv + P;
+      const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
+      const int32_t* ss = sc + P;
+      const double ai = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off);
+      double2 xb[NR];
+      double qq[NR];
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (lo + j * G >= hi) break;
+        const int64_t k = lo + j * G + g;
+        if (k < hi) {
+          const int c = sc[j * G + g];
+          const int s = FULL ? c : ss[j * G + g];
+          xb[j] = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
+        }
+      }
+      double dot = 0.0;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (lo + j * G >= hi) break;
+        const int64_t k = lo + j * G + g;
+        if (k < hi) {
+          dot = fma(sv[j * G + g], xb[j].x, dot);
+          qq[j] = sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
+        }
+      }
+      for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
+        const int c = ld_nc_i32(p.cols + k);
+        const int s = FULL ? c : ld_nc_i32(p.eslot + k);
+        const double2 v = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
+        dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
+        qs[k - lo - P] = ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
+      }
+      dot = group_sum<G>(dot, gmask);
+      const double da = -1.0 / (1.0 + exp(dot)) - ai;
+      const double ngam = -p.gamma;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (lo + j * G >= hi) break;
+        const int64_t k = lo + j * G + g;
+        if (k < hi) {
+          const int c = sc[j * G + g];
+          const int s = FULL ? c : ss[j * G + g];
+          const double a = sv[j * G + g];
+          const double dx = ngam * fma(da, a, qq[j]);
+          if (s >= 0) {
+            atomicAdd(&pend[s].x, dx);
+            if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
+          } else {
+            double* xv = &p.xa[(int64_t)c * p.S].x;
+            red_add(xv, dx);
+            if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+          }
+        }
+      }
+      for (int64_t k = lo + P + g; k < hi; k += G) {
+        const int c = ld_nc_i32(p.cols + k);
+        const int s = FULL ? c : ld_nc_i32(p.eslot + k);
+        const double a = ld_nc_f64(p.vals + k);
+        const double dx = ngam * fma(da, a, qs[k - lo - P]);
+        if (s >= 0) {
+          atomicAdd(&pend[s].x, dx);
+          if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
+        } else {
+          double* xv = &p.xa[(int64_t)c * p.S].x;
+          red_add(xv, dx);
+          if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+        }
+      }
+      if (g == 0) {
+        if (!p.frozen) red_add(p.alpha + i, da);
+        if (p.visits) atomicAdd(p.visits + i, 1);
+        if (p.ov != nullptr) {
+          if (++ov_local == 100) {
+            atomicAdd(p.ov, 100ull);
+            ov_local = 0;
+          }
+          if (ov_meas) {
+            unsigned long long c1;
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(c1) : "l"(p.ov));
+            const unsigned long long o = c1 - ov_c0;
+            ov_sum += o;
+            ov_cnt += 1;
+            ov_max = max(ov_max, o);
+          }
+        }
+      }
+      if (t + W >= tend) break;
+      // advance: this stage is free (every lane is past its reads of it); refill it with
+      // the row of sample m + KS (bounds in the ring) and fetch the bounds of m + 2KS
+      __syncwarp(gmask);
+      const uint64_t mf = m + KS;
+      const int rf = rs + KS >= SM::NB ? rs + KS - SM::NB : rs + KS;  // slot of m + KS
+      if (((mf + KS) & (uint64_t)(G - 1)) == 0) draw_batch(mf + KS);
+      if (t_first + mf * W < tend) {
+        const int64_t* nb = ring + 4 * rf;
+        const int64_t nlo = nb[0], nhi = nb[1], ni = nb[2];
+        fetch_bounds(mf + KS, rs);  // slot of m + 2KS == slot of m
+        issue_row_copy_c<G, NR, FULL>(gbase, stage, p.cols, p.eslot, p.vals, p.dv, p.alpha + ni, nlo,
+                                      nhi, g);
+      } else {
+        cp_async_commit();
+      }
+      t += W;
+      stage = (stage + 1 == KS) ? 0 : stage + 1;
+      rs = (rs + 1 == SM::NB) ? 0 : rs + 1;
+    }
+    cp_async_wait_all();
+    if (p.ov != nullptr && g == 0 && ov_cnt > 0) {
+      atomicAdd(p.ov + 1, ov_sum);
+      atomicAdd(p.ov + 2, ov_cnt);
+      atomicMax(p.ov + 3, ov_max);
+    }
+  }
+  __syncwarp(gmask);
+  if (g == 0) atomic_add_cluster_s32(done0, 1);
+  cluster_sync_all();  // matches the comm warps': they then flush pend
+  cluster_sync_all();
+}
+
+// ---------------------------------------------------------------------------
 // A9: objective / gradient (Section 4.1).  Deterministic: fixed grid, fixed
 // per-group row order, fixed-order block partials.
 // Per row: m_i = a~_i . x, loss_i = softplus(-m_i) = log(1+exp(-b_i a_i.x)),
 // sigma~_i = -1/(1+exp(m_i)) (so sigma_i a_i = sigma~_i a~_i).
-template <int G>
+// A9 margins over row tiles (see "Row tiles" above): m_i = a~_i . x per row by a
+// segmented warp reduction, then loss_i = softplus(-m_i), sigma~_i.
 __global__ void __launch_bounds__(256)
 margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
               const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
               double* __restrict__ sig, double* __restrict__ block_loss) {
-  __shared__ double grp_loss[256 / G];
-  const int lane = threadIdx.x & 31, g = lane & (G - 1);
-  const unsigned gmask =
-      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
-  const int gib = threadIdx.x / G;
-  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
+  __shared__ double rsum[8][32];
+  __shared__ double wl[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / G) + gib; i < n; i += groups) {
-    const int64_t lo = rowptr[i], hi = rowptr[i + 1];
-    double m = 0.0;
-    for (int64_t k = lo + g; k < hi; k += G) m = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m);
-    m = group_sum<G>(m, gmask);
-    // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
-    const double loss = fmax(-m, 0.0) + log1p(exp(-fabs(m)));
-    acc += loss;
-    if (sig != nullptr && g == 0) sig[i] = -1.0 / (1.0 + exp(m));
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * 32 < n; tile += nwarps) {
+    const int64_t r0 = tile * 32;
+    const int nr = (int)((n - r0) < 32 ? (n - r0) : 32);
+    const bool row = lane < nr;
+    const int64_t lo = row ? rowptr[r0 + lane] : 0;
+    const int64_t base = __shfl_sync(0xffffffffu, lo, 0);
+    const int64_t end = rowptr[r0 + nr];
+    const int rel = (int)((row ? lo : end) - base);
+    rsum[wib][lane] = 0.0;
+    __syncwarp();
+#pragma unroll 4
+    for (int64_t e0 = base; e0 < end; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool in = e < end;
+      const double prod = in ? vals[e] * __ldg(x + (int64_t)xs * cols[e]) : 0.0;
+      const int j = tile_row_of((int)(e - base), rel, nr);
+      bool head;
+      const double sm = seg_sum_head(prod, in ? j : 32 + lane, &head);
+      if (in && head) rsum[wib][j] += sm;
+    }
+    __syncwarp();
+    if (row) {
+      const double mu = rsum[wib][lane];
+      // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
+      acc += fmax(-mu, 0.0) + log1p(exp(-fabs(mu)));
+      if (sig != nullptr) sig[r0 + lane] = -1.0 / (1.0 + exp(mu));
+    }
+    __syncwarp();
   }
-  if (g == 0) grp_loss[gib] = acc;
+  acc = group_sum<32>(acc, 0xffffffffu);
+  if (lane == 0) wl[wib] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int j = 0; j < 256 / G; ++j) s += grp_loss[j];
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += wl[j];
     block_loss[blockIdx.x] = s;
   }
 }

@@ -250,8 +250,9 @@ def _epochs_to(p, f_star, runner, tol=1e-6, max_epochs=60):
 
 
 @gpu
-@pytest.mark.parametrize("conc,repl", [(1, 0), (4, 0), (16, 0), (16, 1), (64, 4)])
-def test_async_c1_epochs_within_1p5x_oracle(conc, repl):
+@pytest.mark.parametrize("conc,repl,comb", [(1, 0, 0.0), (4, 0, 0.0), (16, 0, 0.0), (16, 1, 0.0), (64, 4, 0.0),
+                                            (16, 0, 1e-300), (64, 0, 1e-300), (64, 0, 0.1)])
+def test_async_c1_epochs_within_1p5x_oracle(conc, repl, comb):
     m = asaga_mod()
     p = datagen.make("c1")
     fs = _fstar(p)
@@ -264,7 +265,7 @@ def test_async_c1_epochs_within_1p5x_oracle(conc, repl):
         return oracle.objective(p, p.y, p.lam, st.x)
 
     e_or = _epochs_to(p, fs, orun)
-    a = m.Asaga.from_problem(p, g, concurrency=conc, smem_replica_refresh=repl)
+    a = m.Asaga.from_problem(p, g, concurrency=conc, smem_replica_refresh=repl, combine_min_freq=comb)
 
     def grun(k):
         a.run(k, SEED)
@@ -275,10 +276,11 @@ def test_async_c1_epochs_within_1p5x_oracle(conc, repl):
 
 
 @gpu
-@pytest.mark.parametrize("bulk,split,repl", [(0.0, 0.0, 0), (0.5, 0.0, 0), (1e-300, 0.0, 0), (0.0, 0.3, 0),
-                                             (0.0, 1e-300, 0), (0.0, 0.0, 1), (0.5, 0.0, 4)])
+@pytest.mark.parametrize("bulk,split,repl,comb", [(0.0, 0.0, 0, 0.0), (0.5, 0.0, 0, 0.0), (1e-300, 0.0, 0, 0.0),
+                                                  (0.0, 0.3, 0, 0.0), (0.0, 1e-300, 0, 0.0), (0.0, 0.0, 1, 0.0),
+                                                  (0.5, 0.0, 4, 0.0), (0.0, 0.0, 0, 1e-300), (0.0, 0.0, 0, 0.02)])
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
-def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl):
+def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl, comb):
     """Every t is processed exactly once (visit histogram == oracle's stream histogram,
     bit-exact) and, once quiescent, abar == (1/n) sum alpha_i a_i (no lost update)."""
     import scipy.sparse
@@ -286,9 +288,15 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl):
     m = asaga_mod()
     p = SUBSETS[name]()
     T = 5 * p.n + 12345
+    if comb == 1e-300 and p.d > 4096:
+        pytest.skip("every feature combined needs d <= 4096")
     a = m.Asaga.from_problem(p, gamma_of(p), record_samples=True, bulk_scatter_min_freq=bulk,
-                             hot_split_min_freq=split, smem_replica_refresh=repl)
+                             hot_split_min_freq=split, smem_replica_refresh=repl, combine_min_freq=comb)
     assert a.stats()["smem_replica"] == (1 if repl and p.d <= 4096 else 0)
+    if comb > 0:
+        counts, _ = a.profile()
+        want_hot = int(np.sum(counts >= comb * p.n)) if comb > 1e-200 else int(np.sum(counts > 0))
+        assert a.stats()["combine_hot"] == want_hot > 0
     a.run(T, SEED)
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
@@ -302,7 +310,8 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl):
 
 
 @gpu
-def test_async_fixed_point_is_stationary():
+@pytest.mark.parametrize("comb", [0.0, 1e-300, 0.1])
+def test_async_fixed_point_is_stationary(comb):
     """P9 on the GPU: at the optimum state every (async) update is zero."""
     import scipy.sparse
 
@@ -313,7 +322,7 @@ def test_async_fixed_point_is_stationary():
     xs = st.x
     alpha = -p.y / (1.0 + np.exp(p.y * (A @ xs)))
     ab = A.T @ alpha / p.n
-    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=32)
+    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=32, combine_min_freq=comb)
     a.set_state(xs, alpha, ab, 0)
     a.run(10 * p.n, SEED)
     x = a.get_state()[0]
@@ -374,6 +383,18 @@ def test_errors():
         m.Asaga(ok["indptr"], ok["indices"], ok["data"], ok["y"], 2, 0.5, 1.0,
                 bulk_scatter_min_freq=0.5, hot_split_min_freq=0.5)
     assert ei.value.name == "ASAGA_E_INVALID_ARG"
+    for kw in (dict(combine_min_freq=0.5, bulk_scatter_min_freq=0.5), dict(combine_min_freq=2.0),
+               dict(combine_min_freq=0.5, combine_cluster=9)):
+        with pytest.raises(E) as ei:
+            m.Asaga(ok["indptr"], ok["indices"], ok["data"], ok["y"], 2, 0.5, 1.0, **kw)
+        assert ei.value.name == "ASAGA_E_INVALID_ARG", kw
+    # more hot features than a block holds (every one of 5000 features is used)
+    nb = 5000
+    big_ptr = np.arange(nb + 1, dtype=np.int64)
+    with pytest.raises(E) as ei:
+        m.Asaga(big_ptr, np.arange(nb, dtype=np.int32), np.ones(nb), np.ones(nb), nb, 0.5, 1.0,
+                combine_min_freq=1e-300)
+    assert ei.value.name == "ASAGA_E_INVALID_ARG" and "combine_min_freq" in str(ei.value)
     a = mk()
     with pytest.raises(E) as ei:
         a.sample_counts()
@@ -519,9 +540,8 @@ def test_bench_operating_point_c2_full_size_properties():
     m = asaga_mod()
     p = datagen.make("c2")
     op = bench.OPERATING_POINT["c2"]
-    a = m.Asaga.from_problem(p, op["gscale"] * gamma_of(p), concurrency=op["W"],
-                             bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
-                             smem_replica_refresh=op["repl"], record_samples=True)
+    a = m.Asaga.from_problem(p, op["gscale"] * gamma_of(p), concurrency=op["W"], record_samples=True,
+                             **bench.asaga_options(op))
     fs = []
     for _ in range(3):
         a.run(p.n, SEED)

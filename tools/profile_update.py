@@ -1,6 +1,6 @@
 """Drive the update kernel for ncu: one warm-up launch, then one measured launch.
 
-    ncu --set full -k regex:asaga_update -s 1 -c 1 python tools/profile_update.py c3 --conc 512
+    ncu --set full -k regex:asaga_(update|combine) -s 1 -c 1 python tools/profile_update.py c3 --conc 512
 """
 import argparse
 import os
@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
     ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
+    ap.add_argument("--comb", type=float, default=0.0, help="combine_min_freq")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -31,7 +32,7 @@ def main():
     a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc,
               bulk_scatter_min_freq=args.bulk,
               hot_split_min_freq=args.split,
-              smem_replica_refresh=args.repl)
+              smem_replica_refresh=args.repl, combine_min_freq=args.comb)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     T = args.updates or p.n
     a.run(T, datagen.SAMPLE_SEED)  # warm-up launch

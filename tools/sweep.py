@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
     ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
+    ap.add_argument("--comb", type=float, default=0.0, help="combine_min_freq")
+    ap.add_argument("--cluster", type=int, default=0, help="combine_cluster")
+    ap.add_argument("--lanes", type=int, default=0, help="lanes_per_sample")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -45,7 +48,8 @@ def main():
     A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
     base = Asaga(*A, p.d, p.lam, 1.0, bulk_scatter_min_freq=args.bulk,
               hot_split_min_freq=args.split,
-              smem_replica_refresh=args.repl)
+              smem_replica_refresh=args.repl, combine_min_freq=args.comb,
+              combine_cluster=args.cluster, lanes_per_sample=args.lanes)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     for W in [int(c) for c in args.conc.split(",")]:
@@ -65,7 +69,8 @@ def main():
                 a.run_async(step, datagen.SAMPLE_SEED)
                 e1.record(stream)
                 f = a.objective()
-                upd_ms += e0.elapsed_time(e1)
+                last_ms = e0.elapsed_time(e1)
+                upd_ms += last_ms
                 fs.append(f - fstar)
                 if not np.isfinite(f) or f - fstar > 10:
                     ep = "diverged"
@@ -74,9 +79,12 @@ def main():
                     ep = j / 10
                     break
             st = a.stats()
-            r = {"cfg": args.cfg, "W": st["concurrency"], "gamma_scale": sc, "epochs_to_tol": ep,
+            r = {"cfg": args.cfg, "W": st["concurrency"], "comb_H": st["combine_hot"], "cluster": st["combine_cluster"],
+                 "blocks": st["combine_blocks"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "epochs_to_tol": ep,
                  "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
                  "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
+            if st["combine_passes"]:
+                r["comm_pass_us"] = last_ms * 1e3 * st["combine_blocks"] / st["combine_passes"]
             results.append(r)
             print(json.dumps(r), flush=True)
     if args.out:
