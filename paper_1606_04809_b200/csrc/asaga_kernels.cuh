@@ -105,7 +105,7 @@ __device__ __forceinline__ double group_sum(double v, unsigned mask) {
 
 // ---------------------------------------------------------------------------
 // A0 + A1: validation, label folding, column counts, squared row norms.
-enum : int { ERR_ROW_BOUNDS = 0, ERR_EMPTY_ROW, ERR_INDEX_RANGE, ERR_INDEX_ORDER,
+enum : int { ERR_ENDS = 0, ERR_ROW_BOUNDS, ERR_EMPTY_ROW, ERR_INDEX_RANGE, ERR_INDEX_ORDER,
              ERR_NONFINITE, ERR_LABEL, ERR_COUNT };
 
 struct IngestParams {
@@ -124,132 +124,6 @@ struct IngestParams {
   int64_t n, d, nnz;
   int smem_hist;          // 1: per-block shared histogram of all d columns
 };
-
-// One pass over the caller's CSR: validate (errors carry the first bad row), copy
-// rowptr / cols / y into the context, fold b_i into the values, count n_v
-// (shared-memory histogram when d fits, flushed once per block), max ||a_i||^2
-// and the longest row.  Rows go to G-lane groups; each element is read once (the
-// previous index for the order check comes from a shuffle).
-template <int G>
-__global__ void __launch_bounds__(512) ingest_kernel(IngestParams p) {
-  extern __shared__ int32_t hist[];
-  __shared__ double blk_max[32];
-  __shared__ long long blk_len[32];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane & (G - 1);
-  const unsigned gmask =
-      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
-  if (p.smem_hist) {
-    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
-    __syncthreads();
-  }
-  double my_max = 0.0;
-  long long my_len = 0;
-  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / G);
-  // U rows per group in flight: their bounds, labels and first chunk are loaded before
-  // any of them is processed (one row at a time left the pass latency-bound)
-  constexpr int U = 4;
-  for (int64_t i0 = (int64_t)blockIdx.x * (blockDim.x / G) + threadIdx.x / G; i0 < p.n; i0 += U * groups) {
-    int64_t lo_u[U], hi_u[U];
-    double b_u[U];
-    int32_t c_u[U];
-    double v_u[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = i0 + u * groups;
-      lo_u[u] = i < p.n ? p.indptr[i] : 0;
-      hi_u[u] = i < p.n ? p.indptr[i + 1] : 0;
-      b_u[u] = i < p.n ? p.y[i] : 1.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = lo_u[u] + g;
-      const bool ok = lo_u[u] >= 0 && hi_u[u] <= p.nnz && k < hi_u[u];
-      c_u[u] = ok ? p.indices[k] : INT32_MAX;
-      v_u[u] = ok ? p.data[k] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-    const int64_t i = i0 + u * groups;
-    if (i >= p.n) break;  // group-uniform
-    const int64_t lo = lo_u[u], hi = hi_u[u];
-    if (g == 0) {
-      p.rowptr_out[i] = lo;
-      if (i == p.n - 1) p.rowptr_out[p.n] = hi;
-    }
-    if (lo < 0 || hi > p.nnz || hi < lo) {
-      if (g == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
-      continue;
-    }
-    if (hi == lo) {
-      if (g == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
-      continue;
-    }
-    my_len = max(my_len, (long long)(hi - lo));
-    const double b = b_u[u];
-    if (g == 0) {
-      p.y_out[i] = b;
-      if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
-    }
-    double sq = 0.0;
-    bool bad_range = false, bad_order = false, bad_val = false;
-    int carry = -1;  // last index of the previous chunk (group-uniform)
-    for (int64_t base = lo; base < hi; base += G) {
-      const int64_t k = base + g;
-      const bool in = k < hi;
-      const int32_t c = base == lo ? c_u[u] : (in ? p.indices[k] : INT32_MAX);
-      const double v = base == lo ? v_u[u] : (in ? p.data[k] : 0.0);
-      int prev = __shfl_up_sync(gmask, c, 1, G);
-      if (g == 0) prev = carry;
-      if (in) {
-        bad_range |= (c < 0) || ((int64_t)c >= p.d);
-        bad_order |= (base + g > lo) && (prev >= c);
-        bad_val |= !isfinite(v);
-        p.cols_out[k] = c;
-        p.vals[k] = b * v;
-        sq = fma(v, v, sq);
-        if (c >= 0 && (int64_t)c < p.d) {
-          if (p.smem_hist) atomicAdd(&hist[c], 1);
-          else atomicAdd(&p.counts[c], 1);
-        }
-      }
-      carry = __shfl_sync(gmask, c, G - 1, G);
-    }
-    if (__any_sync(gmask, bad_range) && g == 0)
-      atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
-    if (__any_sync(gmask, bad_order) && g == 0)
-      atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
-    if (__any_sync(gmask, bad_val) && g == 0)
-      atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
-    sq = group_sum<G>(sq, gmask);
-    my_max = fmax(my_max, sq);
-    }
-  }
-  // block maxima (warp shuffles, then one atomic per block)
-  for (int off = 16; off > 0; off >>= 1) {
-    my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
-    my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
-  }
-  if (lane == 0) {
-    blk_max[wib] = my_max;
-    blk_len[wib] = my_len;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    long long L = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      m = fmax(m, blk_max[w]);
-      L = max(L, blk_len[w]);
-    }
-    atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
-    atomicMax(p.max_len, (unsigned long long)L);
-  }
-  if (p.smem_hist) {
-    __syncthreads();
-    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
-      if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Row tiles (A0+A1 ingest, A9 margins).  A warp owns 32 consecutive rows and streams
@@ -286,11 +160,11 @@ __device__ __forceinline__ double seg_sum_head(double v, int key, bool* head) {
 
 // A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
 // values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
-__global__ void __launch_bounds__(256) ingest_tile_kernel(IngestParams p) {
+__global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
   extern __shared__ int32_t hist[];
-  __shared__ double rsq[8][32];
-  __shared__ double blk_max[8];
-  __shared__ long long blk_len[8];
+  __shared__ double rsq[32][32];
+  __shared__ double blk_max[32];
+  __shared__ long long blk_len[32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
@@ -298,6 +172,8 @@ __global__ void __launch_bounds__(256) ingest_tile_kernel(IngestParams p) {
   }
   double my_max = 0.0;
   long long my_len = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (p.indptr[0] != 0 || p.indptr[p.n] != p.nnz))
+    atomicMin(&p.err_row[ERR_ENDS], 0ull);  // indptr[0] = 0 and indptr[n] = nnz
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * 32 < p.n; tile += nwarps) {
     const int64_t r0 = tile * 32;
@@ -973,7 +849,7 @@ __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage,
     const int64_t k = lo + j * G + g;
     if (k < hi) {
       cp_async4(sc + j * G + g, cols + k);
-      if (!FULL) cp_async4(ss + j * G + g, eslot + k);
+      if (!FULL && eslot != nullptr) cp_async4(ss + j * G + g, eslot + k);
       cp_async8(sv + j * G + g, vals + k);
       cp_async8(sd + j * G + g, dv + k);
     }
@@ -1154,7 +1030,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int64_t k = lo + j * G + g;
         if (k < hi) {
           const int c = sc[j * G + g];
-          const int s = FULL ? c : ss[j * G + g];
+          const int s = FULL ? c : (H > 0 ? ss[j * G + g] : -1);
           xb[j] = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
         }
       }
@@ -1170,7 +1046,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       }
       for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
         const int c = ld_nc_i32(p.cols + k);
-        const int s = FULL ? c : ld_nc_i32(p.eslot + k);
+        const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double2 v = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
         qs[k - lo - P] = ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
@@ -1184,7 +1060,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int64_t k = lo + j * G + g;
         if (k < hi) {
           const int c = sc[j * G + g];
-          const int s = FULL ? c : ss[j * G + g];
+          const int s = FULL ? c : (H > 0 ? ss[j * G + g] : -1);
           const double a = sv[j * G + g];
           const double dx = ngam * fma(da, a, qq[j]);
           if (s >= 0) {
@@ -1199,7 +1075,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       }
       for (int64_t k = lo + P + g; k < hi; k += G) {
         const int c = ld_nc_i32(p.cols + k);
-        const int s = FULL ? c : ld_nc_i32(p.eslot + k);
+        const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double a = ld_nc_f64(p.vals + k);
         const double dx = ngam * fma(da, a, qs[k - lo - P]);
         if (s >= 0) {
@@ -1306,6 +1182,64 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
       if (sig != nullptr) sig[r0 + lane] = -1.0 / (1.0 + exp(mu));
     }
     __syncwarp();
+  }
+  acc = group_sum<32>(acc, 0xffffffffu);
+  if (lane == 0) wl[wib] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += wl[j];
+    block_loss[blockIdx.x] = s;
+  }
+}
+
+// A9 margins for short rows (mean <= 32): G lanes per row, a warp streams U batches of
+// 32/G CONSECUTIVE rows (coalesced), the first chunk of every row issued before any
+// reduction.  Per row it costs a few warp instructions instead of the tile kernel's
+// per-chunk binary search and segmented reduction.
+template <int G, int U>
+__global__ void __launch_bounds__(256)
+margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                   const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
+                   double* __restrict__ sig, double* __restrict__ block_loss) {
+  constexpr int RG = 32 / G, RPW = RG * U;  // rows per warp batch / per warp iteration
+  __shared__ double wl[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int q = lane / G, g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  double acc = 0.0;
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * RPW < n; tile += nwarps) {
+    const int64_t r0 = tile * RPW;
+    int64_t lo[U], hi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = r0 + u * RG + q;
+      lo[u] = i < n ? rowptr[i] : 0;
+      hi[u] = i < n ? rowptr[i + 1] : 0;
+    }
+    double m[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = lo[u] + g;
+      m[u] = k < hi[u] ? vals[k] * __ldg(x + (int64_t)xs * cols[k]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll 4
+      for (int64_t k = lo[u] + G + g; k < hi[u]; k += G) m[u] = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = r0 + u * RG + q;
+      const double mu = group_sum<G>(m[u], gmask);
+      if (i < n && g == 0) {
+        // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
+        acc += fmax(-mu, 0.0) + log1p(exp(-fabs(mu)));
+        if (sig != nullptr) sig[i] = -1.0 / (1.0 + exp(mu));
+      }
+    }
   }
   acc = group_sum<32>(acc, 0xffffffffu);
   if (lane == 0) wl[wib] = acc;

@@ -278,7 +278,8 @@ def test_async_c1_epochs_within_1p5x_oracle(conc, repl, comb):
 @gpu
 @pytest.mark.parametrize("bulk,split,repl,comb", [(0.0, 0.0, 0, 0.0), (0.5, 0.0, 0, 0.0), (1e-300, 0.0, 0, 0.0),
                                                   (0.0, 0.3, 0, 0.0), (0.0, 1e-300, 0, 0.0), (0.0, 0.0, 1, 0.0),
-                                                  (0.5, 0.0, 4, 0.0), (0.0, 0.0, 0, 1e-300), (0.0, 0.0, 0, 0.02)])
+                                                  (0.5, 0.0, 4, 0.0), (0.0, 0.0, 0, 1e-300), (0.0, 0.0, 0, 0.02),
+                                                  (0.0, 0.0, 0, 0.9)])
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
 def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl, comb):
     """Every t is processed exactly once (visit histogram == oracle's stream histogram,
@@ -296,7 +297,7 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl, com
     if comb > 0:
         counts, _ = a.profile()
         want_hot = int(np.sum(counts >= comb * p.n)) if comb > 1e-200 else int(np.sum(counts > 0))
-        assert a.stats()["combine_hot"] == want_hot > 0
+        assert a.stats()["combine_hot"] == want_hot  # 0: the pipelined kernel, every feature cold
     a.run(T, SEED)
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
