@@ -306,6 +306,76 @@ __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* 
   }
 }
 
+// Small d (<= 1024 * 4): A1's finish and the combine hot set in ONE block -- D_v, state
+// init, Delta_r, hot flags, their exclusive scan (slots in feature order, as the CUB path
+// gives) and the slot tables -- instead of five launches.
+__global__ void __launch_bounds__(1024)
+profile_small_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
+                     double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
+                     int* __restrict__ max_count, double comb_dmax, int max_h,
+                     int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
+                     int* __restrict__ n_hot) {
+  __shared__ int warp_tot[32];
+  __shared__ int warp_max[32];
+  constexpr int PER = 4;  // features per thread (d <= 4096)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int flag[PER], mine = 0, mx = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int v = threadIdx.x * PER + q;
+    flag[q] = 0;
+    if (v < d) {
+      const int c = counts[v];
+      const double Dv = c > 0 ? (double)n / (double)c : 0.0;
+      xa[(int64_t)v * S] = make_double2(0.0, 0.0);
+      habar[v] = 0.0;
+      D[v] = Dv;
+      mx = max(mx, c);
+      flag[q] = (comb_dmax > 0.0 && Dv > 0.0 && Dv <= comb_dmax) ? 1 : 0;
+      mine += flag[q];
+    }
+  }
+  // block exclusive scan of the per-thread hot counts (features in thread order = id order)
+  int incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 31) warp_tot[wib] = incl;
+  if (lane == 0) warp_max[wib] = mx;
+  __syncthreads();
+  if (wib == 0) {
+    const int nw = (int)(blockDim.x >> 5);
+    int t = lane < nw ? warp_tot[lane] : 0;
+    int m = lane < nw ? warp_max[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, t, off);
+      if (lane >= off) t += o;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (lane < nw) warp_tot[lane] = t;  // inclusive over warps
+    if (lane == 0) *max_count = m;
+    if (lane == 31) *n_hot = t;  // inclusive total (nw <= 32)
+  }
+  __syncthreads();
+  int slot = (wib > 0 ? warp_tot[wib - 1] : 0) + incl - mine;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int v = threadIdx.x * PER + q;
+    if (v < d && slot_of != nullptr) {  // NULL when combining is off
+      const bool hot = flag[q] != 0 && slot < max_h;
+      slot_of[v] = hot ? slot : -1;
+      if (hot) hot_id[slot] = v;
+      slot += flag[q];
+    }
+  }
+}
+
 // Combining: hot features are those with 0 < D_v <= comb_dmax (p_v >= combine_min_freq).
 __global__ void hot_flag_kernel(const double* __restrict__ D, int64_t d, double comb_dmax,
                                 int32_t* __restrict__ flag) {
@@ -1017,6 +1087,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       __syncwarp(gmask);             // lane 0 copied alpha_i and the bounds
       const int64_t* cur = ring + 4 * rs;
       const int64_t lo = cur[0], hi = cur[1], i = cur[2];
+      const int len = (int)(hi - lo);
       const double* sv = reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes);
       const double* sd = sv + P;
       const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
@@ -1026,9 +1097,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       double qq[NR];
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        if (lo + j * G >= hi) break;
-        const int64_t k = lo + j * G + g;
-        if (k < hi) {
+        if (j * G >= len) break;  // group-uniform
+        if (j * G + g < len) {
           const int c = sc[j * G + g];
           const int s = FULL ? c : (H > 0 ? ss[j * G + g] : -1);
           xb[j] = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
@@ -1037,9 +1107,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       double dot = 0.0;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        if (lo + j * G >= hi) break;
-        const int64_t k = lo + j * G + g;
-        if (k < hi) {
+        if (j * G >= len) break;  // group-uniform
+        if (j * G + g < len) {
           dot = fma(sv[j * G + g], xb[j].x, dot);
           qq[j] = sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
         }
@@ -1056,16 +1125,35 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       const double ngam = -p.gamma;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        if (lo + j * G >= hi) break;
-        const int64_t k = lo + j * G + g;
-        if (k < hi) {
+        if (j * G >= len) break;  // group-uniform
+        if (j * G + g < len) {
           const int c = sc[j * G + g];
           const int s = FULL ? c : (H > 0 ? ss[j * G + g] : -1);
           const double a = sv[j * G + g];
-          const double dx = ngam * fma(da, a, qq[j]);
+          double dx = ngam * fma(da, a, qq[j]);
+          double dy = p.frozen ? 0.0 : da * a * p.inv_n;
           if (s >= 0) {
-            atomicAdd(&pend[s].x, dx);
-            if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
+            // groups of this warp that add to the same hot slot in this chunk merge their
+            // adds first (xor partners; only lanes converged here take part)
+            bool mine = true;
+            if (G < 32) {
+              const unsigned am = __activemask();
+#pragma unroll
+              for (int off = G; off < 32; off <<= 1) {
+                const int ps = __shfl_xor_sync(am, mine ? s : -1, off);
+                const double px = __shfl_xor_sync(am, dx, off), py = __shfl_xor_sync(am, dy, off);
+                if (((am >> (lane ^ off)) & 1u) && mine && ps == s) {
+                  if (lane & off) mine = false;
+                  else { dx += px; dy += py; }
+                }
+              }
+            }
+            // (atomicAdd on shared f64 compiles to the ATOMS.CAST.SPIN loop; a hand-written
+            // interleaved CAS pair measured 3x slower)
+            if (mine) {
+              atomicAdd(&pend[s].x, dx);
+              if (dy != 0.0) atomicAdd(&pend[s].y, dy);
+            }
           } else {
             double* xv = &p.xa[(int64_t)c * p.S].x;
             red_add(xv, dx);
