@@ -250,14 +250,14 @@ UpdFn combine_fn(const asaga_ctx* ctx, int lanes, int nr) {
 size_t comb_group_bytes(const asaga_ctx* ctx) {  // CombSmem<G, NR, FULL>::bytes
   const bool full = ctx->comb_H == ctx->d;
   const size_t P = (size_t)ctx->nr * ctx->lanes;
-  const size_t alpha_off = P * (2 * sizeof(double) + sizeof(int32_t) + (full ? 0 : sizeof(int32_t)));
+  const size_t alpha_off = full ? P * (sizeof(double) + sizeof(int32_t)) : P * (2 * sizeof(double) + 2 * sizeof(int32_t));
   const size_t stage = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
   // KS = 3 row stages + a bounds ring of 2 KS 32-byte slots + overflow q slots
   return (3 * stage + 6 * 32 + (size_t)ctx->overflow * sizeof(double) + 15) & ~(size_t)15;
 }
 
-size_t comb_smem(const asaga_ctx* ctx, int nwb) {
-  return (size_t)ctx->comb_H * 2 * 16 + (size_t)nwb * comb_group_bytes(ctx);
+size_t comb_smem(const asaga_ctx* ctx, int nwb) {  // xr, pend, D table, worker groups
+  return (size_t)ctx->comb_H * (2 * 16 + 8) + (size_t)nwb * comb_group_bytes(ctx);
 }
 
 // Combine launch shape: blocks in clusters of C (C blocks share one set of hot-feature
@@ -517,15 +517,18 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
   const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 0;
-  const void* kfn = (const void*)ingest_tile_kernel;
-  constexpr int kIngestBlock = 1024;
+  // short rows: 4 lanes per row over consecutive rows; long rows: 32-row tiles streamed flat
+  const bool short_rows = n > 0 && (double)nnz / (double)n <= 12.0;
+  const void* kfn = short_rows ? (const void*)ingest_rows_kernel<4, 4> : (const void*)ingest_tile_kernel;
+  const int kIngestBlock = short_rows ? 512 : 1024;
+  const int rows_per_warp = short_rows ? 32 : 32;
   // (the attribute is per function, shared by every context: set it on every launch)
   CK(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
   if (ctx->ingest_grid == 0) {  // once per context (n, d fixed)
     int per_sm = 1;
     CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kIngestBlock, hsmem));
     per_sm = std::max(per_sm, 1);
-    const int64_t want = (n + 32 * (kIngestBlock / 32) - 1) / (32 * (kIngestBlock / 32));
+    const int64_t want = (n + rows_per_warp * (kIngestBlock / 32) - 1) / (rows_per_warp * (kIngestBlock / 32));
     ctx->ingest_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
   }
   const int grid = ctx->ingest_grid;
@@ -552,15 +555,12 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
         ctx->comb_flag, ctx->comb_excl, d, kCombMaxH, ctx->slot_of, ctx->hot_id, ctx->flag + 2);
     CK(ctx, cudaGetLastError());
   }
-  expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(
-      ctx->cols, ctx->D, nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, d, ctx->eslot);
-  CK(ctx, cudaGetLastError());
   unsigned long long h[ERR_COUNT + 2];
   int hflag[2] = {0, 0};  // max_v n_v, number of hot features
   CK(ctx, cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   CK(ctx, cudaMemcpyAsync(hflag, ctx->flag + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
-  CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
+  // (flag[1], flag[2] = max n_v, hot count stay: expand_d below reads the hot count)
   static const char* what[ERR_COUNT] = {"indptr[0] must be 0 and indptr[n] must be nnz",
                                         "row pointers out of order or out of [0, nnz]",
                                         "empty row (rows must be non-empty)",
@@ -589,6 +589,13 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
     if (ctx->comb_H == d && d > kCombMaxH)
       return fail(ctx, ASAGA_E_INVALID_ARG, "combine_min_freq=%g selects all %lld features; at most %d fit",
                   ctx->comb_freq, (long long)d, kCombMaxH);
+  }
+  // D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
+  // with every feature hot (which reads D from its block table) streams it with the row
+  if (!(use_combine(ctx) && ctx->comb_H == d)) {
+    expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(
+        ctx->cols, ctx->D, nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, d, ctx->eslot);
+    CK(ctx, cudaGetLastError());
   }
   return configure_update(ctx);
 }
@@ -809,6 +816,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.cols = ctx->cols;
   p.vals = ctx->vals;
   p.dv = ctx->dv;
+  p.D = ctx->D;
   p.xa = ctx->xa;
   p.S = ctx->S;
   p.habar = ctx->habar;

@@ -269,6 +269,127 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
   }
 }
 
+// A0 + A1 for short rows (mean <= 12): G lanes per row, each warp U batches of 32/G
+// CONSECUTIVE rows (coalesced), the bounds, label and first chunk of all of them loaded
+// before any is processed.  Same checks and outputs as ingest_tile_kernel.
+template <int G, int U>
+__global__ void __launch_bounds__(512, 2) ingest_rows_kernel(IngestParams p) {
+  extern __shared__ int32_t hist[];
+  __shared__ double blk_max[16];
+  __shared__ long long blk_len[16];
+  constexpr int RG = 32 / G, RPW = RG * U;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, q = lane / G, g = lane & (G - 1);
+  const unsigned gmask =
+      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
+  if (p.smem_hist) {
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (p.indptr[0] != 0 || p.indptr[p.n] != p.nnz))
+    atomicMin(&p.err_row[ERR_ENDS], 0ull);  // indptr[0] = 0 and indptr[n] = nnz
+  double my_max = 0.0;
+  long long my_len = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * RPW < p.n; tile += nwarps) {
+    const int64_t r0 = tile * RPW;
+    int64_t lo_u[U], hi_u[U];
+    double b_u[U], v_u[U];
+    int32_t c_u[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = r0 + u * RG + q;
+      lo_u[u] = i < p.n ? p.indptr[i] : 0;
+      hi_u[u] = i < p.n ? p.indptr[i + 1] : 0;
+      b_u[u] = i < p.n ? p.y[i] : 1.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = lo_u[u] + g;
+      const bool ok = lo_u[u] >= 0 && hi_u[u] <= p.nnz && k < hi_u[u];
+      c_u[u] = ok ? p.indices[k] : INT32_MAX;
+      v_u[u] = ok ? p.data[k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = r0 + u * RG + q;
+      if (i >= p.n) continue;  // group-uniform
+      const int64_t lo = lo_u[u], hi = hi_u[u];
+      const double b = b_u[u];
+      if (g == 0) {
+        p.rowptr_out[i] = lo;
+        if (i == p.n - 1) p.rowptr_out[p.n] = hi;
+        p.y_out[i] = b;
+        if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
+      }
+      if (lo < 0 || hi > p.nnz || hi < lo) {
+        if (g == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
+        continue;
+      }
+      if (hi == lo) {
+        if (g == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
+        continue;
+      }
+      my_len = max(my_len, (long long)(hi - lo));
+      double sq = 0.0;
+      bool bad_range = false, bad_order = false, bad_val = false;
+      int carry = -1;  // last index of the previous chunk (group-uniform)
+      for (int64_t base = lo; base < hi; base += G) {
+        const int64_t k = base + g;
+        const bool in = k < hi;
+        const int32_t c = base == lo ? c_u[u] : (in ? p.indices[k] : INT32_MAX);
+        const double v = base == lo ? v_u[u] : (in ? p.data[k] : 0.0);
+        int prev = __shfl_up_sync(gmask, c, 1, G);
+        if (g == 0) prev = carry;
+        if (in) {
+          bad_range |= (c < 0) || ((int64_t)c >= p.d);
+          bad_order |= (k > lo) && (prev >= c);
+          bad_val |= !isfinite(v);
+          p.cols_out[k] = c;
+          p.vals[k] = b * v;
+          sq = fma(v, v, sq);
+          if (c >= 0 && (int64_t)c < p.d) {
+            if (p.smem_hist) atomicAdd(&hist[c], 1);
+            else atomicAdd(&p.counts[c], 1);
+          }
+        }
+        carry = __shfl_sync(gmask, c, G - 1, G);
+      }
+      if (__any_sync(gmask, bad_range) && g == 0)
+        atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+      if (__any_sync(gmask, bad_order) && g == 0)
+        atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+      if (__any_sync(gmask, bad_val) && g == 0)
+        atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+      sq = group_sum<G>(sq, gmask);
+      my_max = fmax(my_max, sq);
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
+    my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
+  }
+  if (lane == 0) {
+    blk_max[wib] = my_max;
+    blk_len[wib] = my_len;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    long long L = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      m = fmax(m, blk_max[w]);
+      L = max(L, blk_len[w]);
+    }
+    atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
+    atomicMax(p.max_len, (unsigned long long)L);
+  }
+  if (p.smem_hist) {
+    __syncthreads();
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
+      if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
+  }
+}
+
 // A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
 __global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa,
                                int S, double* __restrict__ habar, double* __restrict__ D, int64_t d,
@@ -424,7 +545,8 @@ struct UpdateParams {
   const int64_t* rowptr;
   const int32_t* cols;
   const double* vals;   // folded a~
-  const double* dv;     // D_{c_k} per stored entry
+  const double* dv;     // D_{c_k} per stored entry (not read by the FULL combine kernel)
+  const double* D;      // D_v (combine kernel: the hot features' table)
   double2* xa;          // {x_v, abar_v} at xa[v * S]
   int S;                // pair stride
   double* habar;        // abar_v of hot-split features (entries with dv < 0)
@@ -826,9 +948,10 @@ template <int G, int NR, bool FULL>
 struct CombSmem {
   static constexpr int P = NR * G;
   static constexpr int KS = 3;  // row stages: rows are copied KS samples ahead
-  // per stage: fp64 value, fp64 D, int32 column, int32 slot (!FULL), then alpha_i
-  static constexpr size_t alpha_off = (size_t)P * (2 * sizeof(double) + sizeof(int32_t) +
-                                                   (FULL ? 0 : sizeof(int32_t)));
+  // per stage: fp64 value, [fp64 D, !FULL], int32 column, [int32 slot, !FULL], then alpha_i
+  // (FULL: every feature has a slot and D_v comes from the block's table, not the stream)
+  static constexpr size_t alpha_off = FULL ? (size_t)P * (sizeof(double) + sizeof(int32_t))
+                                           : (size_t)P * (2 * sizeof(double) + 2 * sizeof(int32_t));
   static constexpr size_t stage_bytes = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
   // bounds ring: {lo, hi, i} of samples fetched 2 KS ahead (cp.async, no register waits)
   static constexpr int NB = 2 * KS;
@@ -910,8 +1033,8 @@ __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage,
   unsigned char* sb = base + stage * CombSmem<G, NR, FULL>::stage_bytes;
   if (g == 0) cp_async8(sb + CombSmem<G, NR, FULL>::alpha_off, alpha_i);
   double* sv = reinterpret_cast<double*>(sb);
-  double* sd = sv + P;
-  int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
+  double* sd = sv + P;  // !FULL only
+  int32_t* sc = reinterpret_cast<int32_t*>(sv + (FULL ? P : 2 * P));
   int32_t* ss = sc + P;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
@@ -921,7 +1044,7 @@ __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage,
       cp_async4(sc + j * G + g, cols + k);
       if (!FULL && eslot != nullptr) cp_async4(ss + j * G + g, eslot + k);
       cp_async8(sv + j * G + g, vals + k);
-      cp_async8(sd + j * G + g, dv + k);
+      if (!FULL) cp_async8(sd + j * G + g, dv + k);
     }
   }
   cp_async_commit();
@@ -935,13 +1058,15 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
   const int H = p.H;
   double2* xr = reinterpret_cast<double2*>(smem_raw);
   double2* pend = xr + H;
-  unsigned char* stage_base = smem_raw + (size_t)H * 2 * sizeof(double2);
+  double* Ds = reinterpret_cast<double*>(pend + H);  // FULL: D_v of every feature
+  unsigned char* stage_base = smem_raw + (size_t)H * (2 * sizeof(double2) + sizeof(double));
   const int nwb = p.nwb;  // worker groups in this block (nwb * G is a multiple of 32)
   const unsigned crank = cluster_ctarank(), csize = cluster_nctarank();
   for (int s = threadIdx.x; s < H; s += blockDim.x) {
     const int64_t v = FULL ? s : p.hot_id[s];
     xr[s] = ld_relaxed2(p.xa + v * p.S);
     pend[s] = make_double2(0.0, 0.0);
+    Ds[s] = p.D[v];
   }
   if (threadIdx.x == 0) done = 0;
   cluster_sync_all();  // every block's replica and counter exist before any remote access
@@ -1089,8 +1214,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       const int64_t lo = cur[0], hi = cur[1], i = cur[2];
       const int len = (int)(hi - lo);
       const double* sv = reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes);
-      const double* sd = sv + P;
-      const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
+      const double* sd = sv + P;  // !FULL only
+      const int32_t* sc = reinterpret_cast<const int32_t*>(sv + (FULL ? P : 2 * P));
       const int32_t* ss = sc + P;
       const double ai = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off);
       double2 xb[NR];
@@ -1110,7 +1235,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         if (j * G >= len) break;  // group-uniform
         if (j * G + g < len) {
           dot = fma(sv[j * G + g], xb[j].x, dot);
-          qq[j] = sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
+          qq[j] = (FULL ? Ds[sc[j * G + g]] : sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
         }
       }
       for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
@@ -1118,7 +1243,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double2 v = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
-        qs[k - lo - P] = ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
+        qs[k - lo - P] = (FULL ? Ds[c] : ld_nc_f64(p.dv + k)) * fma(p.lambda_, v.x, v.y);
       }
       dot = group_sum<G>(dot, gmask);
       const double da = -1.0 / (1.0 + exp(dot)) - ai;
