@@ -204,12 +204,24 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     int carry = -1;
     bool bad_range = false, bad_order = false, bad_val = false;
     int first_bad_range = INT32_MAX, first_bad_order = INT32_MAX, first_bad_val = INT32_MAX;
-#pragma unroll 2
-    for (int64_t e0 = base; e0 < end; e0 += 32) {
+    // 4 chunks (128 entries) are loaded before any is processed: loads in flight
+    for (int64_t e00 = base; e00 < end; e00 += 128) {
+    int32_t cq[4];
+    double vq[4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int64_t e = e00 + 32 * qq + lane;
+      cq[qq] = e < end ? p.indices[e] : INT32_MAX;
+      vq[qq] = e < end ? p.data[e] : 0.0;
+    }
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int64_t e0 = e00 + 32 * qq;
+      if (e0 >= end) break;  // warp-uniform
       const int64_t e = e0 + lane;
       const bool in = e < end;
-      const int32_t c = in ? p.indices[e] : INT32_MAX;
-      const double v = in ? p.data[e] : 0.0;
+      const int32_t c = cq[qq];
+      const double v = vq[qq];
       const int off = (int)(e - base);
       const int j = tile_row_of(off, rel, nr);
       const int rs = __shfl_sync(0xffffffffu, rel, j);
@@ -235,6 +247,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
       bool head;
       const double sq = seg_sum_head(in ? v * v : 0.0, in ? j : 32 + lane, &head);
       if (in && head) rsq[wib][j] += sq;
+    }
     }
     if (bad_range) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)(r0 + first_bad_range));
     if (bad_order) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)(r0 + first_bad_order));
