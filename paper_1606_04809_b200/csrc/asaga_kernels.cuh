@@ -1217,7 +1217,9 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
     unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
     int ov_local = 0, ov_iter = 0;
     int stage = 0, rs = 0;  // row stage and bounds-ring slot of sample m
-    for (uint64_t m = 0;; ++m) {
+    // this worker's samples: t_first + mW < tend  (32-bit counts from here on)
+    const int nsamp = (int)((tend - t_first + W - 1) / W);
+    for (int m = 0;; ++m) {
       const bool ov_meas = p.ov != nullptr && (ov_iter++ % p.ov_every) == 0;
       unsigned long long ov_c0 = 0;
       if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
@@ -1251,15 +1253,17 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           qq[j] = (FULL ? Ds[sc[j * G + g]] : sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
         }
       }
-      for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
+      for (int kk = P + g; kk < len; kk += G) {  // long rows only
+        const int64_t k = lo + kk;
         const int c = ld_nc_i32(p.cols + k);
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double2 v = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
-        qs[k - lo - P] = (FULL ? Ds[c] : ld_nc_f64(p.dv + k)) * fma(p.lambda_, v.x, v.y);
+        qs[kk - P] = (FULL ? Ds[c] : ld_nc_f64(p.dv + k)) * fma(p.lambda_, v.x, v.y);
       }
       dot = group_sum<G>(dot, gmask);
-      const double da = -1.0 / (1.0 + exp(dot)) - ai;
+      // sigma~ = -1/(1+exp(m)); the correctly rounded reciprocal equals the IEEE division
+      const double da = -__drcp_rn(1.0 + exp(dot)) - ai;
       const double ngam = -p.gamma;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
@@ -1299,11 +1303,12 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           }
         }
       }
-      for (int64_t k = lo + P + g; k < hi; k += G) {
+      for (int kk = P + g; kk < len; kk += G) {
+        const int64_t k = lo + kk;
         const int c = ld_nc_i32(p.cols + k);
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double a = ld_nc_f64(p.vals + k);
-        const double dx = ngam * fma(da, a, qs[k - lo - P]);
+        const double dx = ngam * fma(da, a, qs[kk - P]);
         if (s >= 0) {
           atomicAdd(&pend[s].x, dx);
           if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
@@ -1331,17 +1336,17 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           }
         }
       }
-      if (t + W >= tend) break;
+      if (m + 1 >= nsamp) break;
       // advance: this stage is free (every lane is past its reads of it); refill it with
       // the row of sample m + KS (bounds in the ring) and fetch the bounds of m + 2KS
       __syncwarp(gmask);
-      const uint64_t mf = m + KS;
+      const int mf = m + KS;
       const int rf = rs + KS >= SM::NB ? rs + KS - SM::NB : rs + KS;  // slot of m + KS
-      if (((mf + KS) & (uint64_t)(G - 1)) == 0) draw_batch(mf + KS);
-      if (t_first + mf * W < tend) {
+      if (((mf + KS) & (G - 1)) == 0) draw_batch((uint64_t)(mf + KS));
+      if (mf < nsamp) {
         const int64_t* nb = ring + 4 * rf;
         const int64_t nlo = nb[0], nhi = nb[1], ni = nb[2];
-        fetch_bounds(mf + KS, rs);  // slot of m + 2KS == slot of m
+        fetch_bounds((uint64_t)(mf + KS), rs);  // slot of m + 2KS == slot of m
         issue_row_copy_c<G, NR, FULL>(gbase, stage, p.cols, p.eslot, p.vals, p.dv, p.alpha + ni, nlo,
                                       nhi, g);
       } else {
