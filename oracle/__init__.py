@@ -86,6 +86,12 @@ def _load():
                                             _F64P]),
             "oracle_svrg_inner": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                          u64, u64, u64, _F64P, _F64P, _F64P]),
+            "oracle_dense_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, f64, f64, u64, u64,
+                                         u64, _F64P, _F64P, _F64P]),
+            "oracle_lagged_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, f64, f64, u64, u64,
+                                          u64, _F64P, _F64P, _F64P]),
+            "oracle_alg1_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
+                                        u64, u64, u64, _F64P, _F64P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -289,3 +295,36 @@ def svrg_inner(A, y, lam, gamma, seed, t0: int, T: int, s, mu, x: np.ndarray, D=
                               _p(y, _F64P), _p(D, _F64P), lam, gamma, seed, t0, T,
                               _p(s, _F64P), _p(mu, _F64P), _p(x, _F64P))
     return x
+
+
+# --------------------------------------------------------------------------- NEXT-4
+def _serial(fn, A, y, lam, gamma, seed, T, state, with_D):
+    n, d, indptr, indices, data = _csr(A)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if state is None:
+        state = State(n, d)
+    args = [n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P), _p(y, _F64P)]
+    if with_D:
+        args.append(_p(reweight(n, column_counts(A)), _F64P))
+    args += [lam, gamma, seed, state.t, T, _p(state.x, _F64P), _p(state.alpha, _F64P)]
+    if fn != "oracle_alg1_saga":
+        args.append(_p(state.alpha_bar, _F64P))
+    getattr(_load(), fn)(*args)
+    state.t += T
+    return state
+
+
+def dense_saga(A, y, lam, gamma, seed, T: int, state: State | None = None) -> State:
+    """Dense SAGA (Eq. 2) with the l2 term: O(d) per step (NEXT-4, desk scale)."""
+    return _serial("oracle_dense_saga", A, y, lam, gamma, seed, T, state, False)
+
+
+def lagged_saga(A, y, lam, gamma, seed, T: int, state: State | None = None) -> State:
+    """SAGA with lagged (just-in-time) dense updates, App. C (NEXT-4)."""
+    return _serial("oracle_lagged_saga", A, y, lam, gamma, seed, T, state, False)
+
+
+def alg1_saga(A, y, lam, gamma, seed, T: int, state: State | None = None) -> State:
+    """Algorithm 1 run sequentially: abar recomputed from the memory every step (NEXT-4).
+    state.alpha_bar is not maintained (Alg. 1 has no stored abar)."""
+    return _serial("oracle_alg1_saga", A, y, lam, gamma, seed, T, state, True)

@@ -347,3 +347,112 @@ void oracle_svrg_inner(int64_t n, int64_t d, const int64_t* indptr, const int32_
   }
   free(u);
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the paper's other serial algorithms, at desk scale (off the hot path).
+ *
+ * Dense SAGA (Eq. 2) on f_i + (lambda/2)||x||^2: the full gradient
+ * estimate f'_i(x) a_i - alpha_i a_i + abar + lambda x is applied to EVERY
+ * coordinate (O(d) per step); abar_v += dalpha a_iv / n; alpha_i = sigma_i.      */
+void oracle_dense_saga(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                       const double* data, const double* y, double lambda, double gamma,
+                       uint64_t seed, uint64_t t0, uint64_t T, double* x, double* alpha,
+                       double* alpha_bar) {
+  const double inv_n = 1.0 / (double)n;
+  double* g = (double*)malloc(sizeof(double) * (size_t)d);
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double dalpha = oracle_sigma(y[i], z) - alpha[i];
+    for (int64_t v = 0; v < d; ++v) g[v] = alpha_bar[v] + lambda * x[v];
+    for (int64_t k = lo; k < hi; ++k) g[indices[k]] = g[indices[k]] + dalpha * data[k];
+    for (int64_t v = 0; v < d; ++v) x[v] = x[v] - gamma * g[v];
+    for (int64_t k = lo; k < hi; ++k)
+      alpha_bar[indices[k]] = alpha_bar[indices[k]] + dalpha * data[k] * inv_n;
+    alpha[i] = alpha[i] + dalpha;
+  }
+  free(g);
+}
+
+/* SAGA with lagged ("just-in-time") updates (App. C):
+ * the dense part of the step, x_v <- x_v - gamma (abar_v + lambda x_v), is
+ * deferred until x_v is next read.  last[v] = the step up to which x_v is current;
+ * abar_v does not change while v is outside the sampled supports, so k deferred
+ * steps of x <- r x - gamma abar (r = 1 - gamma lambda) collapse to
+ *   x <- r^k x - gamma abar (1 + r + ... + r^(k-1)),
+ * summed here term by term (no closed-form division: k is small on desk data).
+ * Sequentially this is the dense iteration ("strictly the same"), up to
+ * rounding.  On return every coordinate is brought to t0 + T.       */
+static void oracle_catch_up(int64_t v, uint64_t t, double lambda, double gamma,
+                            uint64_t* last, double* x, const double* alpha_bar) {
+  for (uint64_t s = last[v]; s < t; ++s) x[v] = x[v] - gamma * (alpha_bar[v] + lambda * x[v]);
+  last[v] = t;
+}
+
+void oracle_lagged_saga(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                        const double* data, const double* y, double lambda, double gamma,
+                        uint64_t seed, uint64_t t0, uint64_t T, double* x, double* alpha,
+                        double* alpha_bar) {
+  const double inv_n = 1.0 / (double)n;
+  uint64_t* last = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)d);
+  for (int64_t v = 0; v < d; ++v) last[v] = t0;
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    for (int64_t k = lo; k < hi; ++k) oracle_catch_up(indices[k], t, lambda, gamma, last, x, alpha_bar);
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double dalpha = oracle_sigma(y[i], z) - alpha[i];
+    /* step t on the support: the sparse part plus step t's own dense part */
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      double gv = alpha_bar[v] + lambda * x[v];
+      gv = gv + dalpha * data[k];
+      x[v] = x[v] - gamma * gv;
+      last[v] = t + 1;
+    }
+    for (int64_t k = lo; k < hi; ++k)
+      alpha_bar[indices[k]] = alpha_bar[indices[k]] + dalpha * data[k] * inv_n;
+    alpha[i] = alpha[i] + dalpha;
+  }
+  for (int64_t v = 0; v < d; ++v) oracle_catch_up(v, t0 + T, lambda, gamma, last, x, alpha_bar);
+  free(last);
+}
+
+/* Algorithm 1 (the analysed ASAGA) run sequentially: every step
+ * recomputes [abar]_{S_i} = (1/n) sum_k [alpha_k]_{S_i} from the whole memory
+ * table (line 7; O(nnz) per step -- "too expensive to be practical"), then
+ * dx = -gamma (f'_i(x) - alpha_i + D_i abar) on S_i with the exact l2 term
+ * lambda D_i x of Section 4.2, alpha_i <- f'_i(x) (line 12, overwrite).
+ * In the GLM case alpha_k = (scalar alpha_k) a_k.  Sequentially this equals Sparse
+ * SAGA (whose abar is maintained incrementally), up to rounding.             */
+void oracle_alg1_saga(int64_t n, int64_t d, const int64_t* indptr, const int32_t* indices,
+                      const double* data, const double* y, const double* D, double lambda,
+                      double gamma, uint64_t seed, uint64_t t0, uint64_t T, double* x,
+                      double* alpha) {
+  const double inv_n = 1.0 / (double)n;
+  double* abar = (double*)malloc(sizeof(double) * (size_t)d);
+  for (uint64_t t = t0; t < t0 + T; ++t) {
+    int64_t i = (int64_t)oracle_sample_index(seed, t, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    /* line 7: abar from scratch (all coordinates; only S_i is used) */
+    for (int64_t v = 0; v < d; ++v) abar[v] = 0.0;
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t k = indptr[r]; k < indptr[r + 1]; ++k)
+        abar[indices[k]] = abar[indices[k]] + alpha[r] * data[k];
+    for (int64_t v = 0; v < d; ++v) abar[v] = abar[v] * inv_n;
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) z += data[k] * x[indices[k]];
+    double s = oracle_sigma(y[i], z);
+    double dalpha = s - alpha[i];
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      double u = dalpha * data[k] + D[v] * (abar[v] + lambda * x[v]);
+      x[v] = x[v] - gamma * u;
+    }
+    alpha[i] = s;
+  }
+  free(abar);
+}
