@@ -2,7 +2,8 @@
 
 A "step" = one pass of every SURVEY.md section 8(a) row over one batch of
 synthetic input:
-    A0+A1  asaga_reload_device     validate, fold labels, n_v / D / L     3 kernels
+    A0+A1  asaga_reload_device_async  validate, fold labels, n_v / D / L (non-blocking;
+                                      the validation is read back by A9's call)
     A2-A8  asaga_run_async(n)      one epoch = n ASAGA updates            1 kernel
     A9     asaga_objective_device  f at the new iterate                   2 kernels
 value = n updates / step time (CUDA events on the context's stream, summed
@@ -252,7 +253,7 @@ def main():
 
     def step(evs):
         evs[0].record(stream)
-        a.reload(indptr, indices, data, y)  # A0 + A1
+        a.reload_async(indptr, indices, data, y)  # A0 + A1 (validated at the objective below)
         evs[1].record(stream)
         a.run_async(p.n, seed)  # A2..A8, one epoch
         evs[2].record(stream)

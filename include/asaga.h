@@ -132,6 +132,10 @@ typedef struct {
                             a cluster share one communication pass over distributed shared
                             memory, so the shared state takes one add per hot feature per
                             CLUSTER per pass. */
+  int combine_write_through; /* combining: 1 = the hot features' replica is kept for READS only;
+                            every add goes straight to the shared state (red.global.add.f64),
+                            so the hot lines lose their per-update loads but no add is held
+                            back.  0 (default) = adds are combined per block. */
 } asaga_options;
 
 typedef struct {
@@ -187,6 +191,18 @@ ASAGA_API asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* 
 ASAGA_API asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y);
 ASAGA_API asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A_dev,
                                            const double* y_dev);
+
+/* As asaga_reload_device, but NON-blocking: A0-A1 are enqueued on the context's stream
+ * and the call returns at once (x = 0, alpha = 0, abar = 0, t = 0 as above).  The
+ * validation is read back by the next BLOCKING call on the context (asaga_run,
+ * asaga_objective[_device], asaga_get_state, asaga_stats, ...), which returns its error
+ * (ASAGA_E_BAD_CSR / _BAD_LABEL with the row, as asaga_reload would).  Until then every
+ * asaga_run_async launch is guarded on the device: it does nothing unless the new data is
+ * valid and fits the context's launch shape (same longest-row capacity, same hot set);
+ * if it did not fit, the resolving call returns ASAGA_E_STATE and those runs must be
+ * repeated.  Without a previous successful ingest it behaves as asaga_reload_device. */
+ASAGA_API asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A_dev,
+                                                 const double* y_dev);
 
 /* Process the global update counters t = t0 .. t0+n_updates-1 (t0 = the
  * context's counter, then t0 += n_updates).  Update t uses row

@@ -46,7 +46,7 @@ class Options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("bulk_scatter_min_freq", ctypes.c_double),
                 ("measure_overlap", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double),
                 ("smem_replica_refresh", ctypes.c_int), ("combine_min_freq", ctypes.c_double),
-                ("combine_cluster", ctypes.c_int)]
+                ("combine_cluster", ctypes.c_int), ("combine_write_through", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -76,6 +76,8 @@ ABI_FUNCTIONS = {
     "asaga_reload": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsrView), ctypes.c_void_p]),
     "asaga_reload_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsrView),
                                            ctypes.c_void_p]),
+    "asaga_reload_device_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsrView),
+                                                 ctypes.c_void_p]),
     "asaga_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]),
     "asaga_run_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]),
     "asaga_objective": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _F64P]),
@@ -168,7 +170,8 @@ class Asaga:
                  atomic: bool = True, record_samples: bool = False, device: int = 0,
                  stream=None, bulk_scatter_min_freq: float = 0.0, measure_overlap: int = 0,
                  hot_split_min_freq: float = 0.0, smem_replica_refresh: int = 0,
-                 combine_min_freq: float = 0.0, combine_cluster: int = 0):
+                 combine_min_freq: float = 0.0, combine_cluster: int = 0,
+                 combine_write_through: bool = False):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -192,6 +195,7 @@ class Asaga:
         opt.smem_replica_refresh = int(smem_replica_refresh)
         opt.combine_min_freq = float(combine_min_freq)
         opt.combine_cluster = int(combine_cluster)
+        opt.combine_write_through = int(bool(combine_write_through))
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),
@@ -237,6 +241,15 @@ class Asaga:
                        _ptr(indices), _ptr(data))
         fn = _lib.asaga_reload_device if dev else _lib.asaga_reload
         _check(fn(self._h, ctypes.byref(view), _ptr(y)), self._h)
+
+    def reload_async(self, indptr, indices, data, y) -> None:
+        """Non-blocking device re-ingest (CUDA tensors, which must stay alive until the
+        next blocking call); validation is reported by that call."""
+        assert _is_cuda(indptr), "reload_async takes device (CUDA) arrays"
+        view = CsrView(int(indptr.shape[0]) - 1, self.d, int(indices.shape[0]), _ptr(indptr),
+                       _ptr(indices), _ptr(data))
+        self._keep_async = (indptr, indices, data, y)
+        _check(_lib.asaga_reload_device_async(self._h, ctypes.byref(view), _ptr(y)), self._h)
 
     def run(self, n_updates: int, seed: int) -> None:
         _check(_lib.asaga_run(self._h, int(n_updates), int(seed)), self._h)

@@ -64,7 +64,12 @@ struct asaga_ctx {
   int comb_nwb = 0;            // worker groups per block of the combine kernel
   int comb_csize = 1;          // blocks per cluster of the combine kernel
   int comb_cluster_opt = 0;    // requested cluster size (0 = 1)
+  int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
+  int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
+  unsigned long long* h_ing = nullptr;  // pinned: ingest validation results (ERR_COUNT + 3)
+  cudaEvent_t ev_ing = nullptr;         // recorded after the ingest's readback copies
+  bool ing_pending = false;             // an asynchronous reload awaits ingest_resolve
   long long shape_key[6] = {0, 0, 0, 0, 0, 0};
   int32_t* comb_flag = nullptr;  // d scratch: hot flags, then their exclusive scan
   int32_t* comb_excl = nullptr;
@@ -358,6 +363,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
   ctx->lanes = lanes;
   ctx->nr = nr;
   ctx->overflow = overflow;
+  ctx->row_cap = (int64_t)nr * lanes + overflow;
   const int groups_per_block = kBlock / lanes;
   // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
   // (GroupSmem in asaga_kernels.cuh)
@@ -455,6 +461,8 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
+  CK(ctx, cudaMallocHost(&ctx->h_ing, sizeof(unsigned long long) * (ERR_COUNT + 3)));
+  CK(ctx, cudaEventCreateWithFlags(&ctx->ev_ing, cudaEventDisableTiming));
   if (ctx->comb_freq > 0.0) {
     TRY(dalloc(ctx, &ctx->slot_of, d));
     TRY(dalloc(ctx, &ctx->hot_id, kCombMaxH));
@@ -474,8 +482,8 @@ asaga_status alloc_state(asaga_ctx* ctx) {
 // buffers, values in data_in (the caller's device array, or ctx->vals itself
 // after a host copy -- the fold is elementwise, so in place is safe).  Resets
 // the state to x = 0, alpha = 0, abar = 0, t = 0 (reading R1).
-asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
-                    const double* data_in, const double* y_in) {
+asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
+                            const double* data_in, const double* y_in) {
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
@@ -556,12 +564,37 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
         ctx->comb_flag, ctx->comb_excl, d, kCombMaxH, ctx->slot_of, ctx->hot_id, ctx->flag + 2);
     CK(ctx, cudaGetLastError());
   }
-  unsigned long long h[ERR_COUNT + 2];
-  int hflag[2] = {0, 0};  // max_v n_v, number of hot features
-  CK(ctx, cudaMemcpyAsync(h, scratch, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(ctx, cudaMemcpyAsync(hflag, ctx->flag + 1, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CK(ctx, cudaStreamSynchronize(ctx->stream));
-  // (flag[1], flag[2] = max n_v, hot count stay: expand_d below reads the hot count)
+  // validation results -> pinned host memory; read back by ingest_resolve (now, or at the
+  // next blocking call after an asynchronous reload)
+  CK(ctx, cudaMemcpyAsync(ctx->h_ing, scratch, sizeof(unsigned long long) * (ERR_COUNT + 2),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaMemcpyAsync(ctx->h_ing + ERR_COUNT + 2, ctx->flag + 1, 2 * sizeof(int),
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  CK(ctx, cudaEventRecord(ctx->ev_ing, ctx->stream));
+  return ASAGA_OK;
+}
+
+bool needs_dv(const asaga_ctx* ctx) { return !(use_combine(ctx) && ctx->comb_H == ctx->d); }
+
+// D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
+// with every feature hot (which reads D from its block table) streams it with the row
+asaga_status enqueue_expand(asaga_ctx* ctx) {
+  if (!needs_dv(ctx)) return ASAGA_OK;
+  expand_d_kernel<<<grid_for(ctx, ctx->nnz, kBlock), kBlock, 0, ctx->stream>>>(
+      ctx->cols, ctx->D, ctx->nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, ctx->d, ctx->eslot);
+  CK(ctx, cudaGetLastError());
+  return ASAGA_OK;
+}
+
+// Read back an enqueued ingest's validation: errors (with the first bad row), L, the
+// longest row, Delta_r and the combine hot count.  Blocks on the ingest's event only.
+asaga_status ingest_resolve(asaga_ctx* ctx) {
+  CK(ctx, cudaEventSynchronize(ctx->ev_ing));
+  ctx->ing_pending = false;
+  const unsigned long long* h = ctx->h_ing;
+  int hflag[2];
+  std::memcpy(hflag, h + ERR_COUNT + 2, sizeof(hflag));  // max_v n_v, number of hot features
+  const int64_t d = ctx->d;
   static const char* what[ERR_COUNT] = {"indptr[0] must be 0 and indptr[n] must be nnz",
                                         "row pointers out of order or out of [0, nnz]",
                                         "empty row (rows must be non-empty)",
@@ -571,8 +604,9 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
                                         "label not in {-1, +1}"};
   for (int e = 0; e < ERR_COUNT; ++e) {
     if (h[e] != ULLONG_MAX) {
+      ctx->shape_valid = false;
       asaga_status s = e == ERR_LABEL ? ASAGA_E_BAD_LABEL : ASAGA_E_BAD_CSR;
-      if (e == ERR_ENDS) return fail(ctx, s, "%s (nnz=%lld)", what[e], (long long)nnz);
+      if (e == ERR_ENDS) return fail(ctx, s, "%s (nnz=%lld)", what[e], (long long)ctx->nnz);
       return fail(ctx, s, "row %llu: %s", h[e], what[e]);
     }
   }
@@ -591,14 +625,43 @@ asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* ind
       return fail(ctx, ASAGA_E_INVALID_ARG, "combine_min_freq=%g selects all %lld features; at most %d fit",
                   ctx->comb_freq, (long long)d, kCombMaxH);
   }
-  // D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
-  // with every feature hot (which reads D from its block table) streams it with the row
-  if (!(use_combine(ctx) && ctx->comb_H == d)) {
-    expand_d_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, ctx->stream>>>(
-        ctx->cols, ctx->D, nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, d, ctx->eslot);
+  return ASAGA_OK;
+}
+
+// Blocking A0-A1: enqueue, resolve, per-entry D, launch shape; the run guard opens.
+asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
+                    const double* data_in, const double* y_in) {
+  TRY(ingest_enqueue(ctx, indptr_in, indices_in, data_in, y_in));
+  TRY(ingest_resolve(ctx));
+  TRY(enqueue_expand(ctx));
+  TRY(configure_update(ctx));
+  set_flag_kernel<<<1, 1, 0, ctx->stream>>>(ctx->flag + 3, 1);  // data and launch shape agree
+  CK(ctx, cudaGetLastError());
+  return ASAGA_OK;
+}
+
+// An asynchronous reload's pending validation: resolved by every blocking entry point.
+asaga_status resolve_pending(asaga_ctx* ctx) {
+  if (!ctx->ing_pending) return ASAGA_OK;
+  const bool had_shape = ctx->shape_valid;
+  const long long key_before[6] = {ctx->shape_key[0], ctx->shape_key[1], ctx->shape_key[2],
+                                   ctx->shape_key[3], ctx->shape_key[4], ctx->shape_key[5]};
+  const int H_before = ctx->comb_H;
+  const bool dv_before = needs_dv(ctx);
+  TRY(ingest_resolve(ctx));
+  const bool dv_after = needs_dv(ctx);
+  TRY(configure_update(ctx));
+  const bool same = had_shape && std::memcmp(key_before, ctx->shape_key, sizeof(key_before)) == 0 &&
+                    H_before == ctx->comb_H && dv_before == dv_after;
+  if (!same) {  // the guarded runs enqueued since the reload were skipped on the device
+    if (dv_after && !dv_before) TRY(enqueue_expand(ctx));
+    set_flag_kernel<<<1, 1, 0, ctx->stream>>>(ctx->flag + 3, 1);
     CK(ctx, cudaGetLastError());
+    return fail(ctx, ASAGA_E_STATE,
+                "the asynchronously reloaded data changed the launch profile (longest row / hot set); "
+                "the runs enqueued since the reload were skipped -- run them again");
   }
-  return configure_update(ctx);
+  return ASAGA_OK;
 }
 
 asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -661,6 +724,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
     return fail(ctx, ASAGA_E_INVALID_ARG, "combine_cluster must be in [0, 8] (got %d)", o.combine_cluster);
   }
   ctx->comb_cluster_opt = o.combine_cluster;
+  ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
   if (e != cudaSuccess) return fail(ctx, ASAGA_E_CUDA, "cudaSetDevice(%d): %s", o.device, cudaGetErrorString(e));
@@ -847,6 +911,8 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.hot_id = ctx->hot_id;
   p.eslot = ctx->comb_H > 0 ? ctx->eslot : nullptr;
   p.comm_passes = ctx->comb_freq > 0.0 ? ctx->scratch + ERR_COUNT + 2 : nullptr;
+  p.wt = ctx->comb_wt;
+  p.ok = ctx->flag + 3;  // 0 while an asynchronous reload's data does not fit this launch
   if (p.comm_passes && use_combine(ctx))
     CK(ctx, cudaMemsetAsync(p.comm_passes, 0, sizeof(unsigned long long), ctx->stream));
   if (use_combine(ctx)) {
@@ -909,6 +975,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->smem_replica_refresh = 0;
   opt->combine_min_freq = 0.0;
   opt->combine_cluster = 0;
+  opt->combine_write_through = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -944,6 +1011,7 @@ static asaga_status check_same_shape(asaga_ctx* ctx, const asaga_csr_view* A, co
 asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
   TRY(check_same_shape(ctx, A, y));
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   if (A->indptr[0] != 0 || A->indptr[A->n] != A->nnz)
     return fail(ctx, ASAGA_E_BAD_CSR, "indptr[0] must be 0 and indptr[n] must be nnz (got %lld and %lld, nnz=%lld)",
                 (long long)A->indptr[0], (long long)A->indptr[A->n], (long long)A->nnz);
@@ -962,9 +1030,26 @@ asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double*
 asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
   TRY(check_same_shape(ctx, A, y));
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   // the ingest pass itself checks indptr[0] = 0, indptr[n] = nnz (no extra round trip) and
   // copies rowptr / cols / y into the context (one read each)
   return ingest(ctx, A->indptr, A->indices, A->data, y);
+}
+
+asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
+  TRY(check_same_shape(ctx, A, y));
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));
+  if (!ctx->shape_valid) return ingest(ctx, A->indptr, A->indices, A->data, y);  // no shape to keep
+  TRY(ingest_enqueue(ctx, A->indptr, A->indices, A->data, y));
+  TRY(enqueue_expand(ctx));
+  // the run guard opens on the device iff the data is valid and fits the current launch
+  ingest_check_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag + 1, ctx->row_cap,
+                                                 ctx->comb_freq > 0.0 ? ctx->comb_H : -1, ctx->flag + 3);
+  CK(ctx, cudaGetLastError());
+  ctx->t = 0;
+  ctx->ing_pending = true;
+  return ASAGA_OK;
 }
 
 asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
@@ -976,6 +1061,7 @@ asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) 
 asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
   if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   if (n_updates == 0) return ASAGA_OK;
   TRY(enqueue_run(ctx, n_updates, seed, true));
   CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int), ctx->stream));
@@ -995,6 +1081,7 @@ asaga_status asaga_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
 asaga_status asaga_objective_device(asaga_ctx* ctx, const double* x_dev, double* f_dev) {
   if (!ctx || !f_dev) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_dev is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   if (x_dev) return enqueue_objective(ctx, x_dev, 1, f_dev, nullptr, false, ctx->stream);
   return enqueue_objective(ctx, current_x(ctx), current_xs(ctx), f_dev, nullptr, false, ctx->stream);
 }
@@ -1002,6 +1089,7 @@ asaga_status asaga_objective_device(asaga_ctx* ctx, const double* x_dev, double*
 asaga_status asaga_objective(asaga_ctx* ctx, const double* x, double* f_out) {
   if (!ctx || !f_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or f_out is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   const double* xd = current_x(ctx);
   int xs = current_xs(ctx);
   if (x) {
@@ -1018,6 +1106,7 @@ asaga_status asaga_objective(asaga_ctx* ctx, const double* x, double* f_out) {
 asaga_status asaga_full_grad(asaga_ctx* ctx, const double* x, double* g_out) {
   if (!ctx || !g_out) return fail(ctx, ASAGA_E_INVALID_ARG, "ctx or g_out is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   TRY(ensure_csc(ctx));
   const double* xd = current_x(ctx);
   int xs = current_xs(ctx);
@@ -1036,6 +1125,7 @@ asaga_status asaga_full_grad(asaga_ctx* ctx, const double* x, double* g_out) {
 asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double* out_dev, void* stream) {
   if (!ctx || !x_dev || !out_dev) return fail(ctx, ASAGA_E_INVALID_ARG, "NULL argument");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   TRY(ensure_csc(ctx));
   cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
   TRY(enqueue_objective(ctx, x_dev, 1, nullptr, out_dev + ctx->d, true, s));
@@ -1046,6 +1136,7 @@ asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double*
 asaga_status asaga_get_state(asaga_ctx* ctx, double* x, double* alpha, double* alpha_bar, uint64_t* t) {
   if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   cudaStream_t s = ctx->stream;
   if (x || alpha_bar) {
     unpack_xa_kernel<<<grid_for(ctx, ctx->d, kBlock), kBlock, 0, s>>>(
@@ -1070,6 +1161,7 @@ asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alph
                              const double* alpha_bar, const uint64_t* t) {
   if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   cudaStream_t s = ctx->stream;
   if (x) CK(ctx, cudaMemcpyAsync(ctx->tmp_d, x, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
   if (alpha_bar)
@@ -1092,6 +1184,7 @@ asaga_status asaga_set_state(asaga_ctx* ctx, const double* x, const double* alph
 asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double* D) {
   if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   cudaStream_t s = ctx->stream;
   if (counts)
     CK(ctx, cudaMemcpyAsync(counts, ctx->counts, sizeof(int32_t) * ctx->d, cudaMemcpyDeviceToHost, s));
@@ -1104,6 +1197,7 @@ asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset)
   if (!ctx || !visits) return fail(ctx, ASAGA_E_INVALID_ARG, "NULL argument");
   if (!ctx->visits) return fail(ctx, ASAGA_E_STATE, "context was created without record_samples");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   CK(ctx, cudaMemcpyAsync(visits, ctx->visits, sizeof(int32_t) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
   if (reset) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * ctx->n, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1123,12 +1217,16 @@ asaga_status asaga_set_concurrency(asaga_ctx* ctx, int64_t concurrency) {
   if (concurrency < 0) return fail(ctx, ASAGA_E_INVALID_ARG, "concurrency must be >= 0");
   if (ctx->deterministic) return fail(ctx, ASAGA_E_STATE, "deterministic context has concurrency 1");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   ctx->concurrency_opt = concurrency;
   return configure_update(ctx);
 }
 
-asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out) {
-  if (!ctx || !out) return fail(nullptr, ASAGA_E_INVALID_ARG, "NULL argument");
+asaga_status asaga_stats(const asaga_ctx* cctx, asaga_stats_t* out) {
+  if (!cctx || !out) return fail(nullptr, ASAGA_E_INVALID_ARG, "NULL argument");
+  asaga_ctx* ctx = const_cast<asaga_ctx*>(cctx);  // resolving a pending reload updates L, Delta_r
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));
   out->n = ctx->n;
   out->d = ctx->d;
   out->nnz = ctx->nnz;
@@ -1209,6 +1307,7 @@ asaga_status asaga_set_algorithm(asaga_ctx* ctx, int algorithm) {
   if (algorithm != ASAGA_ALG_ASAGA && algorithm != ASAGA_ALG_KROMAGNON && algorithm != ASAGA_ALG_HOGWILD)
     return fail(ctx, ASAGA_E_INVALID_ARG, "unknown algorithm %d", algorithm);
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   ctx->algorithm = algorithm;
   ctx->snapshot_valid = false;
   if (algorithm == ASAGA_ALG_HOGWILD) {  // HOGWILD's memory is identically zero
@@ -1227,6 +1326,7 @@ asaga_status asaga_snapshot(asaga_ctx* ctx) {
   if (ctx->algorithm != ASAGA_ALG_KROMAGNON)
     return fail(ctx, ASAGA_E_STATE, "asaga_snapshot is the KROMAGNON synchronised phase");
   CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   TRY(ensure_csc(ctx));
   cudaStream_t s = ctx->stream;
   // alpha~_i := sigma~_i(x) (folded memory), abar := (1/n) sum_i alpha~_i a~_i
@@ -1264,6 +1364,8 @@ void asaga_destroy(asaga_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev_ing) cudaEventDestroy(ctx->ev_ing);
+  if (ctx->h_ing) cudaFreeHost(ctx->h_ing);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

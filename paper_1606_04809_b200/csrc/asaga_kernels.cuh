@@ -440,6 +440,19 @@ __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* 
   }
 }
 
+__global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
+
+// asaga_reload_device_async: open the run guard iff the new data is valid (no error row),
+// its longest row fits the launch shape and its hot-feature count is unchanged.
+__global__ void ingest_check_kernel(const unsigned long long* err_and_max, const int* counts_hot,
+                                    int64_t row_cap, int hot_expected, int* ok) {
+  bool good = true;
+  for (int e = 0; e < ERR_COUNT; ++e) good = good && err_and_max[e] == ~0ull;
+  good = good && (int64_t)err_and_max[ERR_COUNT + 1] <= row_cap;
+  if (hot_expected >= 0) good = good && counts_hot[1] == hot_expected;
+  *ok = good ? 1 : 0;
+}
+
 // Small d (<= 1024 * 4): A1's finish and the combine hot set in ONE block -- D_v, state
 // init, Delta_r, hot flags, their exclusive scan (slots in feature order, as the CUB path
 // gives) and the slot tables -- instead of five launches.
@@ -588,6 +601,8 @@ struct UpdateParams {
   const int32_t* hot_id;  // slot -> feature (NULL when every feature is hot: slot = feature)
   const int32_t* eslot;   // per stored entry: slot of its feature, or -1 (cold)
   unsigned long long* comm_passes;  // += communication-warp passes (asaga_stats)
+  int wt;                 // combine_write_through: hot adds go straight to L2 (replica reads only)
+  const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
 };
 
 // cp.async (LDGSTS) helpers: the next sample's row is copied global -> shared
@@ -685,6 +700,7 @@ __device__ unsigned long long g_phase_cycles[12];
 template <int G, int NR, bool DET, int MODE, bool REPL>
 __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   constexpr bool ATOMIC = MODE != 0;
+  if (p.ok != nullptr && *reinterpret_cast<const volatile int*>(p.ok) == 0) return;  // run guard
 #ifdef ASAGA_TIMING
   unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tprev = clock64();
@@ -1066,6 +1082,7 @@ __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage,
 template <int G, int NR, bool FULL>
 __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (p.ok != nullptr && *reinterpret_cast<const volatile int*>(p.ok) == 0) return;  // run guard (whole grid)
   constexpr int P = NR * G;
   __shared__ int done;  // rank 0's copy counts the finished worker groups of the cluster
   const int H = p.H;
@@ -1108,7 +1125,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
             const int64_t v = FULL ? s : p.hot_id[s];
             double2* gp = p.xa + v * p.S;
             double dx = 0.0, dy = 0.0;
-            if (solo) {
+            if (p.wt) {  // write-through: the workers' adds went to L2; refresh only
+            } else if (solo) {
               dx = exch_shared(&pend[s].x);
               dy = exch_shared(&pend[s].y);
             } else {
@@ -1274,7 +1292,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           const double a = sv[j * G + g];
           double dx = ngam * fma(da, a, qq[j]);
           double dy = p.frozen ? 0.0 : da * a * p.inv_n;
-          if (s >= 0) {
+          if (s >= 0 && !p.wt) {
             // groups of this warp that add to the same hot slot in this chunk merge their
             // adds first (xor partners; only lanes converged here take part)
             bool mine = true;
@@ -1309,7 +1327,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double a = ld_nc_f64(p.vals + k);
         const double dx = ngam * fma(da, a, qs[kk - P]);
-        if (s >= 0) {
+        if (s >= 0 && !p.wt) {
           atomicAdd(&pend[s].x, dx);
           if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
         } else {

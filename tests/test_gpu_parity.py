@@ -556,3 +556,78 @@ def test_bench_operating_point_c2_full_size_properties():
     assert rel(ab, A.T @ alpha / p.n) <= 1e-10
     # f at the GPU iterate, recomputed by the oracle, agrees with the GPU's A9 pass
     assert fs[-1] == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+
+
+# ---------------------------------------------------------------------- asynchronous re-ingest
+@gpu
+def test_reload_async_matches_blocking_reload():
+    """asaga_reload_device_async + run: the same deterministic iterate as the blocking
+    reload (bitwise), and the same profile (L, Delta_r) once resolved."""
+    import torch
+
+    m = asaga_mod()
+    p = SUBSETS["c2s"]()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(a).to(dev)
+    A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
+    g = gamma_of(p)
+    a = m.Asaga(*A, p.d, p.lam, g, deterministic=True)
+    a.run(3000, SEED)
+    a.reload(*A)
+    a.run(5000, SEED)
+    ref = a.get_state()
+    st_ref = a.stats()
+    a.run(777, SEED)
+    a.reload_async(*A)
+    a.run_async(5000, SEED)
+    got = a.get_state()
+    for u, v in zip(ref[:3], got[:3]):
+        assert np.array_equal(u, v)
+    assert got[3] == ref[3] == 5000
+    st = a.stats()
+    assert (st["L"], st["delta_r"], st["max_row"]) == (st_ref["L"], st_ref["delta_r"], st_ref["max_row"])
+
+
+@gpu
+def test_reload_async_errors_surface_at_the_next_blocking_call():
+    """Invalid data: the guarded run does nothing and the next blocking call reports the
+    row (as the blocking reload would); data that does not fit the launch shape: the runs
+    are skipped and reported as ASAGA_E_STATE; a blocking reload then recovers."""
+    import torch
+
+    m = asaga_mod()
+    p = SUBSETS["c1"]()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
+    a = m.Asaga(*A, p.d, p.lam, gamma_of(p), concurrency=16)
+    a.run(p.n, SEED)
+    bad_y = p.y.copy()
+    bad_y[17] = 0.5
+    a.reload_async(A[0], A[1], A[2], t(bad_y))
+    a.run_async(p.n, SEED)
+    with pytest.raises(m.AsagaError) as ei:
+        a.get_state()
+    assert ei.value.name == "ASAGA_E_BAD_LABEL" and "row 17" in str(ei.value)
+    a.reload(*A)  # recover (blocking)
+    assert np.all(a.get_state()[0] == 0.0)
+    # same nnz, but row 0 holds every column: longer than the launch shape holds
+    lens = np.diff(p.indptr).astype(np.int64)
+    lens2 = lens.copy()
+    lens2[0] = p.d
+    excess = lens2.sum() - lens.sum()
+    for i in np.argsort(-lens[1:])[:excess] + 1:
+        lens2[i] -= 1
+    assert lens2.sum() == len(p.indices) and lens2.min() >= 1
+    new_ptr = np.concatenate([[0], np.cumsum(lens2)]).astype(np.int64)
+    nc = np.concatenate([np.arange(p.d, dtype=np.int32)] +
+                        [p.indices[p.indptr[i]:p.indptr[i] + lens2[i]] for i in range(1, p.n)])
+    new_data = np.concatenate([np.full(L, 1.0 / np.sqrt(L)) for L in lens2])
+    B = (t(new_ptr), t(nc.astype(np.int32)), t(new_data), A[3])
+    a.reload_async(*B)
+    a.run_async(p.n, SEED)
+    with pytest.raises(m.AsagaError) as ei:
+        a.objective()
+    assert ei.value.name == "ASAGA_E_STATE"
+    a.run(p.n, SEED)  # now configured for the new data
+    assert np.isfinite(a.objective())
