@@ -67,7 +67,8 @@ struct asaga_ctx {
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
-  unsigned long long* h_ing = nullptr;  // pinned: ingest validation results (ERR_COUNT + 3)
+  unsigned long long* h_ing = nullptr;  // mapped pinned: ingest validation results (ERR_COUNT + 3)
+  unsigned long long* h_ing_dev = nullptr;  // ... its device address
   cudaEvent_t ev_ing = nullptr;         // recorded after the ingest's readback copies
   bool ing_pending = false;             // an asynchronous reload awaits ingest_resolve
   long long shape_key[6] = {0, 0, 0, 0, 0, 0};
@@ -461,7 +462,8 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
-  CK(ctx, cudaMallocHost(&ctx->h_ing, sizeof(unsigned long long) * (ERR_COUNT + 3)));
+  CK(ctx, cudaHostAlloc(&ctx->h_ing, sizeof(unsigned long long) * (ERR_COUNT + 3), cudaHostAllocMapped));
+  CK(ctx, cudaHostGetDevicePointer(&ctx->h_ing_dev, ctx->h_ing, 0));
   CK(ctx, cudaEventCreateWithFlags(&ctx->ev_ing, cudaEventDisableTiming));
   if (ctx->comb_freq > 0.0) {
     TRY(dalloc(ctx, &ctx->slot_of, d));
@@ -488,11 +490,9 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
   if (ctx->ov) CK(ctx, cudaMemsetAsync(ctx->ov, 0, 4 * sizeof(unsigned long long), ctx->stream));
-  CK(ctx, cudaMemsetAsync(ctx->counts, 0, sizeof(int32_t) * d, ctx->stream));
-  CK(ctx, cudaMemsetAsync(ctx->alpha, 0, sizeof(double) * n, ctx->stream));
-  CK(ctx, cudaMemsetAsync(scratch, 0xff, sizeof(unsigned long long) * ERR_COUNT, ctx->stream));
-  CK(ctx, cudaMemsetAsync(scratch + ERR_COUNT, 0, sizeof(unsigned long long) * 2, ctx->stream));
-  CK(ctx, cudaMemsetAsync(ctx->flag, 0, sizeof(int) * 4, ctx->stream));
+  ingest_init_kernel<<<grid_for(ctx, std::max(n, d), kBlock), kBlock, 0, ctx->stream>>>(
+      ctx->counts, d, ctx->alpha, n, scratch, ctx->flag);
+  CK(ctx, cudaGetLastError());
   ctx->t = 0;
   ctx->snapshot_valid = false;
   if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
@@ -564,12 +564,15 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
         ctx->comb_flag, ctx->comb_excl, d, kCombMaxH, ctx->slot_of, ctx->hot_id, ctx->flag + 2);
     CK(ctx, cudaGetLastError());
   }
-  // validation results -> pinned host memory; read back by ingest_resolve (now, or at the
-  // next blocking call after an asynchronous reload)
-  CK(ctx, cudaMemcpyAsync(ctx->h_ing, scratch, sizeof(unsigned long long) * (ERR_COUNT + 2),
-                          cudaMemcpyDeviceToHost, ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->h_ing + ERR_COUNT + 2, ctx->flag + 1, 2 * sizeof(int),
-                          cudaMemcpyDeviceToHost, ctx->stream));
+  return ASAGA_OK;
+}
+
+// The validation results -> mapped pinned host memory (read by ingest_resolve now, or at
+// the next blocking call after an asynchronous reload); guard: also set the run guard.
+asaga_status enqueue_report(asaga_ctx* ctx, bool guard) {
+  ingest_report_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag, ctx->h_ing_dev, ctx->row_cap,
+                                                 ctx->comb_freq > 0.0 ? ctx->comb_H : -1, guard ? 1 : 0);
+  CK(ctx, cudaGetLastError());
   CK(ctx, cudaEventRecord(ctx->ev_ing, ctx->stream));
   return ASAGA_OK;
 }
@@ -591,9 +594,11 @@ asaga_status enqueue_expand(asaga_ctx* ctx) {
 asaga_status ingest_resolve(asaga_ctx* ctx) {
   CK(ctx, cudaEventSynchronize(ctx->ev_ing));
   ctx->ing_pending = false;
-  const unsigned long long* h = ctx->h_ing;
-  int hflag[2];
-  std::memcpy(hflag, h + ERR_COUNT + 2, sizeof(hflag));  // max_v n_v, number of hot features
+  const volatile unsigned long long* hv = ctx->h_ing;  // written by the device (mapped)
+  unsigned long long h[ERR_COUNT + 3];
+  for (int e = 0; e < ERR_COUNT + 3; ++e) h[e] = hv[e];
+  const int hflag[2] = {(int)(unsigned)(h[ERR_COUNT + 2] & 0xffffffffu),  // max_v n_v
+                        (int)(unsigned)(h[ERR_COUNT + 2] >> 32)};        // number of hot features
   const int64_t d = ctx->d;
   static const char* what[ERR_COUNT] = {"indptr[0] must be 0 and indptr[n] must be nnz",
                                         "row pointers out of order or out of [0, nnz]",
@@ -632,6 +637,7 @@ asaga_status ingest_resolve(asaga_ctx* ctx) {
 asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
                     const double* data_in, const double* y_in) {
   TRY(ingest_enqueue(ctx, indptr_in, indices_in, data_in, y_in));
+  TRY(enqueue_report(ctx, false));
   TRY(ingest_resolve(ctx));
   TRY(enqueue_expand(ctx));
   TRY(configure_update(ctx));
@@ -1044,9 +1050,7 @@ asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A, 
   TRY(ingest_enqueue(ctx, A->indptr, A->indices, A->data, y));
   TRY(enqueue_expand(ctx));
   // the run guard opens on the device iff the data is valid and fits the current launch
-  ingest_check_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag + 1, ctx->row_cap,
-                                                 ctx->comb_freq > 0.0 ? ctx->comb_H : -1, ctx->flag + 3);
-  CK(ctx, cudaGetLastError());
+  TRY(enqueue_report(ctx, true));
   ctx->t = 0;
   ctx->ing_pending = true;
   return ASAGA_OK;

@@ -442,15 +442,35 @@ __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* 
 
 __global__ void set_flag_kernel(int* flag, int v) { *flag = v; }
 
-// asaga_reload_device_async: open the run guard iff the new data is valid (no error row),
-// its longest row fits the launch shape and its hot-feature count is unchanged.
-__global__ void ingest_check_kernel(const unsigned long long* err_and_max, const int* counts_hot,
-                                    int64_t row_cap, int hot_expected, int* ok) {
+// A0's state reset in one launch (instead of five memsets): n_v = 0, alpha = 0, the error
+// rows = "none", max ||a||^2 = max row = 0, the small flags = 0.
+__global__ void ingest_init_kernel(int32_t* __restrict__ counts, int64_t d, double* __restrict__ alpha,
+                                   int64_t n, unsigned long long* __restrict__ scratch,
+                                   int* __restrict__ flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t v = t0; v < d; v += stride) counts[v] = 0;
+  for (int64_t i = t0; i < n; i += stride) alpha[i] = 0.0;
+  if (t0 < ERR_COUNT) scratch[t0] = ~0ull;
+  if (t0 < 2) scratch[ERR_COUNT + t0] = 0ull;
+  if (t0 < 4) flag[t0] = 0;
+}
+
+// The ingest's report, written straight into mapped pinned host memory (no copies):
+// error rows, max ||a||^2, longest row, max n_v, hot count; and the run guard for an
+// asynchronous reload (valid data that fits the launch shape), when guard != 0.
+__global__ void ingest_report_kernel(const unsigned long long* __restrict__ scratch,
+                                     int* __restrict__ flag, unsigned long long* host_out,
+                                     int64_t row_cap, int hot_expected, int guard) {
   bool good = true;
-  for (int e = 0; e < ERR_COUNT; ++e) good = good && err_and_max[e] == ~0ull;
-  good = good && (int64_t)err_and_max[ERR_COUNT + 1] <= row_cap;
-  if (hot_expected >= 0) good = good && counts_hot[1] == hot_expected;
-  *ok = good ? 1 : 0;
+  for (int e = 0; e < ERR_COUNT + 2; ++e) {
+    host_out[e] = scratch[e];
+    if (e < ERR_COUNT) good = good && scratch[e] == ~0ull;
+  }
+  host_out[ERR_COUNT + 2] = (unsigned long long)(unsigned)flag[1] | ((unsigned long long)(unsigned)flag[2] << 32);
+  good = good && (int64_t)scratch[ERR_COUNT + 1] <= row_cap;
+  if (hot_expected >= 0) good = good && flag[2] == hot_expected;
+  if (guard) flag[3] = good ? 1 : 0;
 }
 
 // Small d (<= 1024 * 4): A1's finish and the combine hot set in ONE block -- D_v, state
