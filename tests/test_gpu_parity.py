@@ -631,3 +631,29 @@ def test_reload_async_errors_surface_at_the_next_blocking_call():
     assert ei.value.name == "ASAGA_E_STATE"
     a.run(p.n, SEED)  # now configured for the new data
     assert np.isfinite(a.objective())
+
+
+@gpu
+@pytest.mark.parametrize("name,comb,cluster,wt", [("c2s", 1e-300, 2, False), ("c2s", 1e-300, 4, False),
+                                                  ("c3s", 0.02, 2, False), ("c2s", 1e-300, 1, True),
+                                                  ("c3s", 0.02, 1, True)])
+def test_combine_clusters_and_write_through_keep_every_add(name, comb, cluster, wt):
+    """Cluster-shared combining (DSMEM) and write-through replicas: every t processed once,
+    the quiescent identity abar == (1/n) sum alpha_i a_i, and f falls below log 2 (small
+    step: the property, not the convergence budget, is under test)."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 3 * p.n + 999
+    a = m.Asaga.from_problem(p, gamma_of(p) / 16, record_samples=True, concurrency=256,
+                             combine_min_freq=comb, combine_cluster=cluster, combine_write_through=wt)
+    st = a.stats()
+    assert st["combine_hot"] > 0 and st["combine_cluster"] == cluster
+    a.run(T, SEED)
+    ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
+    assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x)) and a.objective() < np.log(2.0)
