@@ -456,7 +456,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
     CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mfn, kBlock, 0));
     ctx->obj_blocks = ctx->sms * std::max(1, std::min(per_sm, 8));
   }
-  TRY(dalloc(ctx, &ctx->block_loss, ctx->obj_blocks));
+  TRY(dalloc(ctx, &ctx->block_loss, 2 * (size_t)ctx->obj_blocks));  // loss partials, ||x||^2 partials
   TRY(dalloc(ctx, &ctx->scal, 4));
   TRY(dalloc(ctx, &ctx->flag, 4));
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
@@ -524,13 +524,11 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.d = d;
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
-  const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 0;
-  // short rows: 4 lanes per row over consecutive rows; long rows: 32-row tiles streamed flat
-  // (a G-lanes-per-row variant, ingest_rows_kernel, measured 77 us vs 69 us on c2)
-  const bool short_rows = false;
-  const void* kfn = short_rows ? (const void*)ingest_rows_kernel<4, 4> : (const void*)ingest_tile_kernel;
-  const int kIngestBlock = short_rows ? 512 : 1024;
-  const int rows_per_warp = short_rows ? 32 : 32;
+  const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t);
+  // 32-row tiles streamed flat (a G-lanes-per-row variant measured 77 us vs 69 us on c2)
+  const void* kfn = (const void*)ingest_tile_kernel;
+  const int kIngestBlock = 1024;
+  const int rows_per_warp = 32;
   // (the attribute is per function, shared by every context: set it on every launch)
   CK(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
   if (ctx->ingest_grid == 0) {  // once per context (n, d fixed)
@@ -846,16 +844,16 @@ asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, doub
   const double mean = (double)ctx->nnz / (double)ctx->n;
   if (mean <= 12.0)
     margin_rows_kernel<4, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                                 ctx->n, sig, ctx->block_loss);
+                                                                 ctx->n, sig, ctx->block_loss, ctx->d);
   else if (mean <= 24.0)
     margin_rows_kernel<8, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                                 ctx->n, sig, ctx->block_loss);
+                                                                 ctx->n, sig, ctx->block_loss, ctx->d);
   else if (ctx->margin_tiles)
     margin_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs, ctx->n, sig,
-                                                     ctx->block_loss);
+                                                     ctx->block_loss, ctx->d);
   else
     margin_rows_kernel<32, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                                  ctx->n, sig, ctx->block_loss);
+                                                                  ctx->n, sig, ctx->block_loss, ctx->d);
   CK(ctx, cudaGetLastError());
   finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, xs, ctx->d,
                                              ctx->n, ctx->lambda, f_dev, loss_sum_dev);

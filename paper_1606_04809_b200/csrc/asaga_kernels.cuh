@@ -122,7 +122,8 @@ struct IngestParams {
   unsigned long long* max_sq;    // bits of max_i ||a_i||^2 (>= 0 doubles order as u64)
   unsigned long long* max_len;   // longest row
   int64_t n, d, nnz;
-  int smem_hist;          // 1: per-block shared histogram of all d columns
+  int smem_hist;          // 1: per-block shared histogram of all d columns; 0: a per-block
+                          // shared hash cache of kHashSlots columns (the popular ones claim it)
 };
 
 // ---------------------------------------------------------------------------
@@ -158,6 +159,8 @@ __device__ __forceinline__ double seg_sum_head(double v, int key, bool* head) {
   return v;
 }
 
+constexpr int kHashLog = 12, kHashSlots = 1 << kHashLog;  // ingest hash cache (32 KiB)
+
 // A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
 // values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
 __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
@@ -166,10 +169,17 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
   __shared__ double blk_max[32];
   __shared__ long long blk_len[32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int32_t* hkey = hist;                  // !smem_hist: hash cache keys (-1 = free) ...
+  int32_t* hcnt = hist + kHashSlots;     // ... and counts
   if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
-    __syncthreads();
+  } else {
+    for (int k = threadIdx.x; k < kHashSlots; k += blockDim.x) {
+      hkey[k] = -1;
+      hcnt[k] = 0;
+    }
   }
+  __syncthreads();
   double my_max = 0.0;
   long long my_len = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0 && (p.indptr[0] != 0 || p.indptr[p.n] != p.nnz))
@@ -240,8 +250,20 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         p.cols_out[e] = c;
         p.vals[e] = bj * v;
         if (!br) {
-          if (p.smem_hist) atomicAdd(&hist[c], 1);
-          else atomicAdd(&p.counts[c], 1);
+          if (p.smem_hist) {
+            atomicAdd(&hist[c], 1);
+          } else {
+            // n_v: a Zipf-popular column would take ~1e6 serialised global atomics (c4: 4.8 ms
+            // of the ingest); the first column to hash into a free slot keeps it per block
+            const int slot = (int)(((unsigned)c * 2654435761u) >> (32 - kHashLog));
+            int k = hkey[slot];
+            if (k == -1) {
+              const int prev = atomicCAS(&hkey[slot], -1, c);
+              k = prev == -1 ? c : prev;
+            }
+            if (k == c) atomicAdd(&hcnt[slot], 1);
+            else atomicAdd(&p.counts[c], 1);
+          }
         }
       }
       bool head;
@@ -275,131 +297,13 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
     atomicMax(p.max_len, (unsigned long long)L);
   }
-  if (p.smem_hist) {
-    __syncthreads();
-    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
-      if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
-  }
-}
-
-// A0 + A1 for short rows (mean <= 12): G lanes per row, each warp U batches of 32/G
-// CONSECUTIVE rows (coalesced), the bounds, label and first chunk of all of them loaded
-// before any is processed.  Same checks and outputs as ingest_tile_kernel.
-template <int G, int U>
-__global__ void __launch_bounds__(512, 2) ingest_rows_kernel(IngestParams p) {
-  extern __shared__ int32_t hist[];
-  __shared__ double blk_max[16];
-  __shared__ long long blk_len[16];
-  constexpr int RG = 32 / G, RPW = RG * U;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, q = lane / G, g = lane & (G - 1);
-  const unsigned gmask =
-      (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
-  if (p.smem_hist) {
-    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
-    __syncthreads();
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (p.indptr[0] != 0 || p.indptr[p.n] != p.nnz))
-    atomicMin(&p.err_row[ERR_ENDS], 0ull);  // indptr[0] = 0 and indptr[n] = nnz
-  double my_max = 0.0;
-  long long my_len = 0;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; tile * RPW < p.n; tile += nwarps) {
-    const int64_t r0 = tile * RPW;
-    int64_t lo_u[U], hi_u[U];
-    double b_u[U], v_u[U];
-    int32_t c_u[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = r0 + u * RG + q;
-      lo_u[u] = i < p.n ? p.indptr[i] : 0;
-      hi_u[u] = i < p.n ? p.indptr[i + 1] : 0;
-      b_u[u] = i < p.n ? p.y[i] : 1.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t k = lo_u[u] + g;
-      const bool ok = lo_u[u] >= 0 && hi_u[u] <= p.nnz && k < hi_u[u];
-      c_u[u] = ok ? p.indices[k] : INT32_MAX;
-      v_u[u] = ok ? p.data[k] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t i = r0 + u * RG + q;
-      if (i >= p.n) continue;  // group-uniform
-      const int64_t lo = lo_u[u], hi = hi_u[u];
-      const double b = b_u[u];
-      if (g == 0) {
-        p.rowptr_out[i] = lo;
-        if (i == p.n - 1) p.rowptr_out[p.n] = hi;
-        p.y_out[i] = b;
-        if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
-      }
-      if (lo < 0 || hi > p.nnz || hi < lo) {
-        if (g == 0) atomicMin(&p.err_row[ERR_ROW_BOUNDS], (unsigned long long)i);
-        continue;
-      }
-      if (hi == lo) {
-        if (g == 0) atomicMin(&p.err_row[ERR_EMPTY_ROW], (unsigned long long)i);
-        continue;
-      }
-      my_len = max(my_len, (long long)(hi - lo));
-      double sq = 0.0;
-      bool bad_range = false, bad_order = false, bad_val = false;
-      int carry = -1;  // last index of the previous chunk (group-uniform)
-      for (int64_t base = lo; base < hi; base += G) {
-        const int64_t k = base + g;
-        const bool in = k < hi;
-        const int32_t c = base == lo ? c_u[u] : (in ? p.indices[k] : INT32_MAX);
-        const double v = base == lo ? v_u[u] : (in ? p.data[k] : 0.0);
-        int prev = __shfl_up_sync(gmask, c, 1, G);
-        if (g == 0) prev = carry;
-        if (in) {
-          bad_range |= (c < 0) || ((int64_t)c >= p.d);
-          bad_order |= (k > lo) && (prev >= c);
-          bad_val |= !isfinite(v);
-          p.cols_out[k] = c;
-          p.vals[k] = b * v;
-          sq = fma(v, v, sq);
-          if (c >= 0 && (int64_t)c < p.d) {
-            if (p.smem_hist) atomicAdd(&hist[c], 1);
-            else atomicAdd(&p.counts[c], 1);
-          }
-        }
-        carry = __shfl_sync(gmask, c, G - 1, G);
-      }
-      if (__any_sync(gmask, bad_range) && g == 0)
-        atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
-      if (__any_sync(gmask, bad_order) && g == 0)
-        atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
-      if (__any_sync(gmask, bad_val) && g == 0)
-        atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
-      sq = group_sum<G>(sq, gmask);
-      my_max = fmax(my_max, sq);
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    my_max = fmax(my_max, __shfl_xor_sync(0xffffffffu, my_max, off));
-    my_len = max(my_len, __shfl_xor_sync(0xffffffffu, my_len, off));
-  }
-  if (lane == 0) {
-    blk_max[wib] = my_max;
-    blk_len[wib] = my_len;
-  }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    long long L = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      m = fmax(m, blk_max[w]);
-      L = max(L, blk_len[w]);
-    }
-    atomicMax(p.max_sq, (unsigned long long)__double_as_longlong(m));
-    atomicMax(p.max_len, (unsigned long long)L);
-  }
   if (p.smem_hist) {
-    __syncthreads();
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
       if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
+  } else {
+    for (int k = threadIdx.x; k < kHashSlots; k += blockDim.x)
+      if (hkey[k] >= 0 && hcnt[k]) atomicAdd(&p.counts[hkey[k]], hcnt[k]);
   }
 }
 
@@ -1412,14 +1316,40 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
 // per-group row order, fixed-order block partials.
 // Per row: m_i = a~_i . x, loss_i = softplus(-m_i) = log(1+exp(-b_i a_i.x)),
 // sigma~_i = -1/(1+exp(m_i)) (so sigma_i a_i = sigma~_i a~_i).
+// A9 block partials in a fixed order: block_out[b] = this block's loss sum and
+// block_out[gridDim.x + b] = its share of ||x||^2 (x strided over the whole grid).
+__device__ __forceinline__ void block_partials(double acc, const double* __restrict__ x, int xs, int64_t d,
+                                               double* __restrict__ block_out, double* wl, double* wq) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double sq = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d; v += (int64_t)gridDim.x * blockDim.x)
+    sq = fma(x[(int64_t)xs * v], x[(int64_t)xs * v], sq);
+  acc = group_sum<32>(acc, 0xffffffffu);
+  sq = group_sum<32>(sq, 0xffffffffu);
+  if (lane == 0) {
+    wl[wib] = acc;
+    wq[wib] = sq;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0, q = 0.0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) {
+      s += wl[j];
+      q += wq[j];
+    }
+    block_out[blockIdx.x] = s;
+    block_out[gridDim.x + blockIdx.x] = q;
+  }
+}
+
 // A9 margins over row tiles (see "Row tiles" above): m_i = a~_i . x per row by a
 // segmented warp reduction, then loss_i = softplus(-m_i), sigma~_i.
 __global__ void __launch_bounds__(256)
 margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
               const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
-              double* __restrict__ sig, double* __restrict__ block_loss) {
+              double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
   __shared__ double rsum[8][32];
-  __shared__ double wl[8];
+  __shared__ double wl[8], wq[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   double acc = 0.0;
@@ -1452,14 +1382,7 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
     }
     __syncwarp();
   }
-  acc = group_sum<32>(acc, 0xffffffffu);
-  if (lane == 0) wl[wib] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += wl[j];
-    block_loss[blockIdx.x] = s;
-  }
+  block_partials(acc, x, xs, d, block_loss, wl, wq);
 }
 
 // A9 margins for short rows (mean <= 32): G lanes per row, a warp streams U batches of
@@ -1470,9 +1393,9 @@ template <int G, int U>
 __global__ void __launch_bounds__(256)
 margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                    const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
-                   double* __restrict__ sig, double* __restrict__ block_loss) {
+                   double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
   constexpr int RG = 32 / G, RPW = RG * U;  // rows per warp batch / per warp iteration
-  __shared__ double wl[8];
+  __shared__ double wl[8], wq[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int q = lane / G, g = lane & (G - 1);
   const unsigned gmask =
@@ -1510,25 +1433,21 @@ margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict
       }
     }
   }
-  acc = group_sum<32>(acc, 0xffffffffu);
-  if (lane == 0) wl[wib] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) s += wl[j];
-    block_loss[blockIdx.x] = s;
-  }
+  block_partials(acc, x, xs, d, block_loss, wl, wq);
 }
 
-// Single block: f = (sum block_loss) / n + lambda/2 ||x||^2; also raw loss sum.
+// Single block: f = (sum of loss partials) / n + lambda/2 (sum of ||x||^2 partials); also the
+// raw loss sum.  (x, xs, d unused: the partials come from the margin kernel.)
 __global__ void __launch_bounds__(1024)
 finish_objective_kernel(const double* __restrict__ block_loss, int nblocks,
                         const double* __restrict__ x, int xs, int64_t d, int64_t n, double lambda_,
                         double* __restrict__ f_out, double* __restrict__ loss_sum_out) {
   __shared__ double s_loss[1024], s_sq[1024];
-  double a = 0.0, b = 0.0;
-  for (int j = threadIdx.x; j < nblocks; j += blockDim.x) a += block_loss[j];
-  for (int64_t v = threadIdx.x; v < d; v += blockDim.x) b = fma(x[xs * v], x[xs * v], b);
+  double a = 0.0, b = 0.0;  // the margin kernel's block partials: loss sums, then ||x||^2 shares
+  for (int j = threadIdx.x; j < nblocks; j += blockDim.x) {
+    a += block_loss[j];
+    b += block_loss[nblocks + j];
+  }
   s_loss[threadIdx.x] = a;
   s_sq[threadIdx.x] = b;
   __syncthreads();
