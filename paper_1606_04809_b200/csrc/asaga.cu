@@ -449,7 +449,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
      // context, so the block partials are summed in a fixed order: deterministic f)
     const double mean = n ? (double)nnz / (double)n : 1.0;
     ctx->margin_tiles = getenv("ASAGA_MARGIN_TILES") != nullptr;  // experiment: 32-row tiles for long rows
-    const void* mfn = mean <= 12.0 ? (const void*)margin_rows_kernel<4, 4>
+    const void* mfn = mean <= 16.0 ? (const void*)margin_thread_kernel
                       : mean <= 24.0 ? (const void*)margin_rows_kernel<8, 4>
                       : ctx->margin_tiles ? (const void*)margin_kernel : (const void*)margin_rows_kernel<32, 4>;
     int per_sm = 1;
@@ -525,7 +525,8 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
   const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t);
-  // 32-row tiles streamed flat (a G-lanes-per-row variant measured 77 us vs 69 us on c2)
+  // 32-row tiles per warp streamed flat (measured against a G-lanes-per-row variant, 77 vs
+  // 69 us on c2, and a thread-per-row variant, 102 us: uncoalesced, 1.3x the DRAM bytes)
   const void* kfn = (const void*)ingest_tile_kernel;
   const int kIngestBlock = 1024;
   const int rows_per_warp = 32;
@@ -842,9 +843,9 @@ asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, doub
   double* sig = want_sig ? ctx->sig : nullptr;
   // short rows: G lanes per row (G ~ mean/3); long rows: 32-row tiles streamed flat
   const double mean = (double)ctx->nnz / (double)ctx->n;
-  if (mean <= 12.0)
-    margin_rows_kernel<4, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
-                                                                 ctx->n, sig, ctx->block_loss, ctx->d);
+  if (mean <= 16.0)
+    margin_thread_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
+                                                            ctx->n, sig, ctx->block_loss, ctx->d);
   else if (mean <= 24.0)
     margin_rows_kernel<8, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
                                                                  ctx->n, sig, ctx->block_loss, ctx->d);

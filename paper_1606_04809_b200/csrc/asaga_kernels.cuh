@@ -1342,6 +1342,25 @@ __device__ __forceinline__ void block_partials(double acc, const double* __restr
   }
 }
 
+// A9 margins for short rows (mean <= 16): one thread per row (see ingest_thread_kernel).
+__global__ void __launch_bounds__(256)
+margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
+                     const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
+                     double* __restrict__ sig, double* __restrict__ block_out, int64_t d) {
+  __shared__ double wl[8], wq[8];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = rowptr[i], hi = rowptr[i + 1];
+    double m = 0.0;
+#pragma unroll 4
+    for (int64_t k = lo; k < hi; ++k) m = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m);
+    // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
+    acc += fmax(-m, 0.0) + log1p(exp(-fabs(m)));
+    if (sig != nullptr) sig[i] = -1.0 / (1.0 + exp(m));
+  }
+  block_partials(acc, x, xs, d, block_out, wl, wq);
+}
+
 // A9 margins over row tiles (see "Row tiles" above): m_i = a~_i . x per row by a
 // segmented warp reduction, then loss_i = softplus(-m_i), sigma~_i.
 __global__ void __launch_bounds__(256)
