@@ -917,6 +917,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.eslot = ctx->comb_H > 0 ? ctx->eslot : nullptr;
   p.comm_passes = ctx->comb_freq > 0.0 ? ctx->scratch + ERR_COUNT + 2 : nullptr;
   p.wt = ctx->comb_wt;
+  p.split = ctx->hot_dmax > 0.0 ? 1 : 0;
   p.ok = ctx->flag + 3;  // 0 while an asynchronous reload's data does not fit this launch
   if (p.comm_passes && use_combine(ctx))
     CK(ctx, cudaMemsetAsync(p.comm_passes, 0, sizeof(unsigned long long), ctx->stream));

@@ -526,6 +526,7 @@ struct UpdateParams {
   const int32_t* eslot;   // per stored entry: slot of its feature, or -1 (cold)
   unsigned long long* comm_passes;  // += communication-warp passes (asaga_stats)
   int wt;                 // combine_write_through: hot adds go straight to L2 (replica reads only)
+  int split;              // hot split in use (entries with dv < 0 keep abar in habar)
   const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
 };
 
@@ -581,11 +582,12 @@ __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, c
                                          stage * GroupSmem<G, NR>::stage_bytes);
   double* sd = sv + P;
   int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
+  const int len = (int)(hi - lo);
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
-    if (lo + j * G >= hi) break;  // group-uniform: no predicated-off chunks
+    if (j * G >= len) break;  // group-uniform: no predicated-off chunks
     const int64_t k = lo + j * G + g;
-    if (k < hi) {
+    if (j * G + g < len) {
       cp_async4(sc + j * G + g, cols + k);
       cp_async8(sv + j * G + g, vals + k);
       cp_async8(sd + j * G + g, dv + k);
@@ -655,18 +657,32 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   uint64_t t = p.t0 + (uint64_t)w;
   if (t >= tend) return;
   const uint64_t W = (uint64_t)p.workers;
+  const uint64_t t_first = t;
+  // sample indices in batches of G: lane j draws sample mb + j of this worker (one Philox
+  // per lane per G samples), shuffled out in order (group-uniform calls)
+  int64_t bi = 0;
+  auto draw_batch = [&](uint64_t mb) {
+    const uint64_t ts = t_first + (mb + (uint64_t)g) * W;
+    bi = ts < tend ? sample_row(p.seed, ts, p.n) : 0;
+  };
+  auto sample_of = [&](uint64_t ms) -> int64_t {
+    return __shfl_sync(gmask, bi, (int)(ms & (uint64_t)(G - 1)), G);
+  };
+  static_assert(G >= 4, "a batch covers the prologue's three samples");
+  uint64_t m = 0;  // this worker's sample count
+  draw_batch(0);
   // prologue: current row bounds + its copy; next row bounds; next-next index
-  int64_t i = sample_row(p.seed, t, p.n);
+  int64_t i = sample_of(0);
   int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
   int stage = 0;
   issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, lo, hi, g);
   int64_t in1 = 0, lo1 = 0, hi1 = 0, in2 = 0;
+  in1 = sample_of(1);
+  in2 = sample_of(2);
   if (t + W < tend) {
-    in1 = sample_row(p.seed, t + W, p.n);
     lo1 = __ldg(&p.rowptr[in1]);
     hi1 = __ldg(&p.rowptr[in1 + 1]);
   }
-  if (t + 2 * W < tend) in2 = sample_row(p.seed, t + 2 * W, p.n);
 
   unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
   int ov_local = 0, ov_iter = 0;
@@ -676,6 +692,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     unsigned long long ov_c0 = 0;
     if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
     // ---- pass 1: row entries (shared memory), gathers, dot product
+    const int len = (int)(hi - lo);
     cp_async_wait_all();
     TMARK(0);
     const double* sv = reinterpret_cast<const double*>(gbase + GroupSmem<G, NR>::delta_bytes +
@@ -687,13 +704,13 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     double2 xb[NR];
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      if (lo + j * G >= hi) break;  // group-uniform
+      if (j * G >= len) break;  // group-uniform
       const int64_t k = lo + j * G + g;
-      if (k < hi) {
+      if (j * G + g < len) {
         const int c = sc[j * G + g];
         if (REPL)
           xb[j] = rx[c];
-        else if (sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
+        else if (p.split && sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
           xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c));
         else
           xb[j] = ld_na2(p.xa + (int64_t)c * p.S);
@@ -725,9 +742,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     double dot = 0.0;
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      if (lo + j * G >= hi) break;  // group-uniform
+      if (j * G >= len) break;  // group-uniform
       const int64_t k = lo + j * G + g;
-      if (k < hi) {
+      if (j * G + g < len) {
         dot = fma(sv[j * G + g], xb[j].x, dot);
         qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
       }
@@ -749,7 +766,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #ifdef ASAGA_TIMING
     const double sig = (p.debug_mode & 2) ? -0.5 + 0.0 * dot : -1.0 / (1.0 + exp(dot));
 #else
-    const double sig = -1.0 / (1.0 + exp(dot));
+    const double sig = -__drcp_rn(1.0 + exp(dot));  // correctly rounded: == -1.0 / (1 + e)
 #endif
     const double da = sig - ai;
     const double ngam = -p.gamma;
@@ -763,14 +780,14 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     TMARK(6);
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
-      if (lo + j * G >= hi) break;  // group-uniform
+      if (j * G >= len) break;  // group-uniform
       const int64_t k = lo + j * G + g;
-      if (k < hi) {
+      if (j * G + g < len) {
         const int c = sc[j * G + g];
         const double a = sv[j * G + g];
         const double u = fma(da, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
-        double* abv = sd[j * G + g] < 0.0 ? p.habar + c : xv + 1;  // hot split
+        double* abv = (p.split && sd[j * G + g] < 0.0) ? p.habar + c : xv + 1;  // hot split
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
           dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : da * a * p.inv_n);
         } else if (MODE >= 1) {
@@ -788,9 +805,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       TMARK(8);
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        if (lo + j * G >= hi) break;
+        if (j * G >= len) break;
         const int64_t k = lo + j * G + g;
-        if (k < hi && sd[j * G + g] <= p.bulk_dmax)
+        if (j * G + g < len && sd[j * G + g] <= p.bulk_dmax)
           bulk_red_pair(p.xa + (int64_t)sc[j * G + g] * p.S, dbuf + j * G + g);
       }
       bulk_commit();
@@ -858,7 +875,11 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     t += W;
     i = in1; lo = lo1; hi = hi1;
     in1 = in2; lo1 = lo2; hi1 = hi2;
-    if (t + 2 * W < tend) in2 = sample_row(p.seed, t + 2 * W, p.n);
+    ++m;
+    if (t + 2 * W < tend) {  // group-uniform
+      if (((m + 2) & (uint64_t)(G - 1)) == 0) draw_batch(m + 2);
+      in2 = sample_of(m + 2);
+    }
     stage ^= 1;
   }
   cp_async_wait_all();
