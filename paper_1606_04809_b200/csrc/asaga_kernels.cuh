@@ -1037,14 +1037,27 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
   unsigned char* stage_base = smem_raw + (size_t)H * (2 * sizeof(double2) + sizeof(double));
   const int nwb = p.nwb;  // worker groups in this block (nwb * G is a multiple of 32)
   const unsigned crank = cluster_ctarank(), csize = cluster_nctarank();
-  for (int s = threadIdx.x; s < H; s += blockDim.x) {
-    const int64_t v = FULL ? s : p.hot_id[s];
-    xr[s] = ld_relaxed2(p.xa + v * p.S);
-    pend[s] = make_double2(0.0, 0.0);
-    Ds[s] = p.D[v];
-  }
-  if (threadIdx.x == 0) done = 0;
-  cluster_sync_all();  // every block's replica and counter exist before any remote access
+  const bool solo = csize == 1;  // one block per cluster: block barriers, plain shared memory
+  // The block's hot-slot tables; every thread runs this once, from its role's code, after
+  // a worker has issued its prologue loads (they overlap), then the start barrier.
+  auto init_slots = [&]() {
+    for (int s = threadIdx.x; s < H; s += blockDim.x) {
+      const int64_t v = FULL ? s : p.hot_id[s];
+      xr[s] = ld_relaxed2(p.xa + v * p.S);
+      pend[s] = make_double2(0.0, 0.0);
+      Ds[s] = p.D[v];
+    }
+    if (threadIdx.x == 0) done = 0;
+  };
+  // every block's replica and counter exist before any (remote) access
+  auto start_sync = [&]() {
+    if (solo) asm volatile("bar.sync 2;" ::: "memory");
+    else cluster_sync_all();
+  };
+  auto end_sync = [&]() {
+    if (solo) asm volatile("bar.sync 3;" ::: "memory");
+    else cluster_sync_all();
+  };
   const unsigned done0 = mapa_shared(&done, 0);
 
   if ((int)threadIdx.x >= nwb * G) {
@@ -1054,11 +1067,12 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
     // (one add per hot feature per cluster per pass), re-read the shared pair and store
     // it into every block's replica.
     const int lane = threadIdx.x & 31;
+    init_slots();
+    start_sync();
     const int total = nwb * (int)csize;
     constexpr int B = 4;  // slots per lane per batch (their loads in flight together)
     unsigned long long passes = 0;
     const volatile int* vdone = &done;
-    const bool solo = csize == 1;  // one block per cluster: plain shared-memory operations
     while ((solo ? *vdone : ld_cluster_volatile_s32(done0)) < total) {
       ++passes;
       for (int s0 = (int)crank + (int)csize * lane; s0 < H; s0 += (int)csize * 32 * B) {
@@ -1100,7 +1114,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         }
       }
     }
-    cluster_sync_all();  // every worker of the cluster has finished its adds to pend
+    end_sync();  // every worker of the cluster has finished its adds to pend
     if (lane == 0 && p.comm_passes != nullptr) atomicAdd(p.comm_passes, passes);
     for (int s = (int)crank + (int)csize * lane; s < H; s += (int)csize * 32) {
       const int64_t v = FULL ? s : p.hot_id[s];
@@ -1114,7 +1128,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       if (dx != 0.0) red_add(&gp->x, dx);
       if (dy != 0.0) red_add(&gp->y, dy);
     }
-    cluster_sync_all();  // no block exits while another may still read its pend
+    end_sync();  // no block exits while another may still read its pend
     return;
   }
 
@@ -1134,7 +1148,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
   const uint64_t W = (uint64_t)p.workers;
   const uint64_t t_first = p.t0 + (uint64_t)w;
   uint64_t t = t_first;
-  if (w < p.workers && t < tend) {
+  const bool active = w < p.workers && t < tend;
+  {
     // Pipeline over this worker's samples m = 0, 1, ... (t = t_first + mW), all of it
     // read-only data, so fetching early changes nothing but latency:
     //   the row (+ alpha_i) of sample m + KS is copied at iteration m (KS stages),
@@ -1163,20 +1178,33 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         cp_async8(slot + 1, p.rowptr + is + 1);
       }
     };
-    draw_batch(0);
-#pragma unroll 1
-    for (int k = 0; k < KS; ++k) {  // prologue: rows of samples 0..KS-1, bounds of KS..2KS-1
-      const uint64_t ts = t_first + (uint64_t)k * W;
-      const int64_t is = sample_of((uint64_t)k);
-      fetch_bounds((uint64_t)(k + KS), k + KS);
-      if (ts < tend) {
-        const int64_t l0 = __ldg(&p.rowptr[is]), h0 = __ldg(&p.rowptr[is + 1]);
-        if (g == 0) { ring[4 * k] = l0; ring[4 * k + 1] = h0; ring[4 * k + 2] = is; }
-        issue_row_copy_c<G, NR, FULL>(gbase, k, p.cols, p.eslot, p.vals, p.dv, p.alpha + is, l0, h0, g);
-      } else {
-        cp_async_commit();
+    if (active) {
+      // prologue: rows of samples 0..KS-1 (their bounds loaded together: one round trip),
+      // bounds of KS..2KS-1
+      draw_batch(0);
+      int64_t pis[KS], plo[KS], phi[KS];
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        pis[k] = sample_of((uint64_t)k);
+        const bool in = t_first + (uint64_t)k * W < tend;
+        plo[k] = in ? __ldg(&p.rowptr[pis[k]]) : 0;
+        phi[k] = in ? __ldg(&p.rowptr[pis[k] + 1]) : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        fetch_bounds((uint64_t)(k + KS), k + KS);
+        if (t_first + (uint64_t)k * W < tend) {
+          if (g == 0) { ring[4 * k] = plo[k]; ring[4 * k + 1] = phi[k]; ring[4 * k + 2] = pis[k]; }
+          issue_row_copy_c<G, NR, FULL>(gbase, k, p.cols, p.eslot, p.vals, p.dv, p.alpha + pis[k], plo[k],
+                                        phi[k], g);
+        } else {
+          cp_async_commit();
+        }
       }
     }
+    init_slots();
+    start_sync();
+    if (active) {
     unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
     int ov_local = 0, ov_iter = 0;
     int stage = 0, rs = 0;  // row stage and bounds-ring slot of sample m
@@ -1325,11 +1353,15 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       atomicAdd(p.ov + 2, ov_cnt);
       atomicMax(p.ov + 3, ov_max);
     }
+    }  // active
   }
   __syncwarp(gmask);
-  if (g == 0) atomic_add_cluster_s32(done0, 1);
-  cluster_sync_all();  // matches the comm warps': they then flush pend
-  cluster_sync_all();
+  if (g == 0) {
+    if (solo) atomicAdd(&done, 1);
+    else atomic_add_cluster_s32(done0, 1);
+  }
+  end_sync();  // matches the comm warps': they then flush pend
+  end_sync();
 }
 
 // ---------------------------------------------------------------------------
