@@ -113,6 +113,7 @@ struct asaga_ctx {
   size_t smem = 0;         // dynamic shared memory of a full (kBlock) block
   size_t group_bytes = 0;  // dynamic shared memory per group
   int grid = 1, block = kBlock;
+  int max_tpb = kBlock;    // largest update-kernel block the shared memory allows
   int64_t workers = 1;
   int max_resident_groups = 1;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -337,7 +338,7 @@ int scatter_mode(const asaga_ctx* ctx) {
 void launch_shape(const asaga_ctx* ctx, int64_t workers, int* grid, int* block) {
   const int64_t threads = workers * ctx->lanes;
   int64_t tpb = 32;
-  while (tpb < kBlock && tpb * ctx->sms < threads) tpb *= 2;
+  while (tpb < ctx->max_tpb && tpb * ctx->sms < threads) tpb *= 2;
   *block = (int)tpb;
   *grid = (int)((threads + tpb - 1) / tpb);
 }
@@ -365,7 +366,6 @@ asaga_status configure_update(asaga_ctx* ctx) {
   ctx->nr = nr;
   ctx->overflow = overflow;
   ctx->row_cap = (int64_t)nr * lanes + overflow;
-  const int groups_per_block = kBlock / lanes;
   // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
   // (GroupSmem in asaga_kernels.cuh)
   // (GroupSmem: bulk-scatter source buffer + 2 row stages + overflow q slots)
@@ -400,17 +400,22 @@ asaga_status configure_update(asaga_ctx* ctx) {
     ctx->shape_valid = true;
     return ASAGA_OK;
   }
-  ctx->smem = replica_bytes(ctx) + (size_t)groups_per_block * group_bytes;
+  // blocks of up to kBlock threads, fewer when long rows' overflow slots need the room
+  int tpb_max = kBlock;
+  while (tpb_max > 32 && replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes > 226 * 1024) tpb_max /= 2;
+  ctx->max_tpb = tpb_max;
+  const int gpb = tpb_max / lanes;
+  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes;
   UpdFn fn = update_fn(ctx, lanes, nr);
-  if (ctx->smem > 227 * 1024)
+  if (ctx->smem > 226 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
                 (long long)ctx->max_row);
   CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)ctx->smem));
   int per_sm = 0;
-  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kBlock, ctx->smem));
+  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, tpb_max, ctx->smem));
   per_sm = std::max(per_sm, 1);
-  ctx->max_resident_groups = per_sm * ctx->sms * groups_per_block;
+  ctx->max_resident_groups = per_sm * ctx->sms * gpb;
   int64_t workers;
   if (ctx->deterministic) workers = 1;
   else if (ctx->concurrency_opt > 0) workers = std::min<int64_t>(ctx->concurrency_opt, ctx->max_resident_groups);
@@ -524,10 +529,16 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.d = d;
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
-  const size_t hsmem = ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t);
+  const size_t hist_bytes =
+      ((ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t)) + 15) & ~(size_t)15;
+  // short rows: warp stages (kStageCap entries per warp) when they fit next to the histogram
+  const size_t stage_bytes = 32 * (size_t)kStageCap * (sizeof(double) + sizeof(int32_t));
+  const bool staged = n > 0 && (double)nnz / (double)n <= 16.0 && hist_bytes + stage_bytes <= 200 * 1024;
+  const size_t hsmem = hist_bytes + (staged ? stage_bytes : 0);
+  ip.stage_off = hist_bytes;
   // 32-row tiles per warp streamed flat (measured against a G-lanes-per-row variant, 77 vs
   // 69 us on c2, and a thread-per-row variant, 102 us: uncoalesced, 1.3x the DRAM bytes)
-  const void* kfn = (const void*)ingest_tile_kernel;
+  const void* kfn = staged ? (const void*)ingest_tile_kernel<true> : (const void*)ingest_tile_kernel<false>;
   const int kIngestBlock = 1024;
   const int rows_per_warp = 32;
   // (the attribute is per function, shared by every context: set it on every launch)

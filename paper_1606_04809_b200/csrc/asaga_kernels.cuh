@@ -122,6 +122,7 @@ struct IngestParams {
   unsigned long long* max_sq;    // bits of max_i ||a_i||^2 (>= 0 doubles order as u64)
   unsigned long long* max_len;   // longest row
   int64_t n, d, nnz;
+  size_t stage_off;       // ingest_tile_kernel<true>: byte offset of the warp stages in smem
   int smem_hist;          // 1: per-block shared histogram of all d columns; 0: a per-block
                           // shared hash cache of kHashSlots columns (the popular ones claim it)
 };
@@ -163,14 +164,44 @@ constexpr int kHashLog = 12, kHashSlots = 1 << kHashLog;  // ingest hash cache (
 
 // A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
 // values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
+// STAGED (short rows): a tile whose entries fit kStageCap is copied into the warp's
+// shared stage with coalesced loads, each row is then checked / folded / counted by its
+// OWNER lane from shared memory (the previous index and ||a_i||^2 in registers: a few
+// instructions per entry instead of the flat path's per-chunk row search and segmented
+// reduction), and the tile is written back coalesced.  Larger tiles take the flat path.
+constexpr int kStageCap = 512;  // entries per warp stage (int32 index + fp64 value: 6 KiB)
+
+template <bool STAGED>
 __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
-  extern __shared__ int32_t hist[];
+  extern __shared__ __align__(16) int32_t hist[];
   __shared__ double rsq[32][32];
   __shared__ double blk_max[32];
   __shared__ long long blk_len[32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* hkey = hist;                  // !smem_hist: hash cache keys (-1 = free) ...
   int32_t* hcnt = hist + kHashSlots;     // ... and counts
+  // STAGED: per-warp stages after the histogram (p.stage_off bytes into dynamic smem)
+  double* stage_v = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(hist) + p.stage_off) +
+                    (size_t)wib * kStageCap;
+  int32_t* stage_c = reinterpret_cast<int32_t*>(reinterpret_cast<unsigned char*>(hist) + p.stage_off +
+                                                (size_t)(blockDim.x >> 5) * kStageCap * sizeof(double)) +
+                     (size_t)wib * kStageCap;
+  auto count_col = [&](int c) {
+    if (p.smem_hist) {
+      atomicAdd(&hist[c], 1);
+    } else {
+      // n_v: a Zipf-popular column would take ~1e6 serialised global atomics (c4: 4.8 ms
+      // of the ingest); the first column to hash into a free slot keeps it per block
+      const int slot = (int)(((unsigned)c * 2654435761u) >> (32 - kHashLog));
+      int k = hkey[slot];
+      if (k == -1) {
+        const int prev = atomicCAS(&hkey[slot], -1, c);
+        k = prev == -1 ? c : prev;
+      }
+      if (k == c) atomicAdd(&hcnt[slot], 1);
+      else atomicAdd(&p.counts[c], 1);
+    }
+  };
   if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
   } else {
@@ -209,6 +240,45 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     const int64_t base = __shfl_sync(0xffffffffu, lo, 0);
     const int64_t end = __shfl_sync(0xffffffffu, hi, nr - 1);
     const int rel = (int)((row ? lo : end) - base);
+    if (STAGED && end - base <= kStageCap) {
+      const int cnt = (int)(end - base);
+#pragma unroll 4
+      for (int e = lane; e < cnt; e += 32) {
+        stage_c[e] = p.indices[base + e];
+        stage_v[e] = p.data[base + e];
+      }
+      __syncwarp();
+      if (row) {
+        int prevc = -1;
+        double sq = 0.0;
+        bool br_any = false, bo_any = false, bv_any = false;
+        const int kend = rel + (int)(hi - lo);
+        for (int k = rel; k < kend; ++k) {
+          const int32_t c = stage_c[k];
+          const double v = stage_v[k];
+          const bool br = (c < 0) || ((int64_t)c >= p.d);
+          br_any |= br;
+          bo_any |= prevc >= c;
+          bv_any |= !isfinite(v);
+          prevc = c;
+          stage_v[k] = b * v;
+          sq = fma(v, v, sq);
+          if (!br) count_col(c);
+        }
+        if (br_any) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+        if (bo_any) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+        if (bv_any) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+        my_max = fmax(my_max, sq);
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int e = lane; e < cnt; e += 32) {
+        p.cols_out[base + e] = stage_c[e];
+        p.vals[base + e] = stage_v[e];
+      }
+      __syncwarp();
+      continue;
+    }
     rsq[wib][lane] = 0.0;
     __syncwarp();
     int carry = -1;
@@ -249,22 +319,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         bad_range |= br; bad_order |= bo; bad_val |= bv;
         p.cols_out[e] = c;
         p.vals[e] = bj * v;
-        if (!br) {
-          if (p.smem_hist) {
-            atomicAdd(&hist[c], 1);
-          } else {
-            // n_v: a Zipf-popular column would take ~1e6 serialised global atomics (c4: 4.8 ms
-            // of the ingest); the first column to hash into a free slot keeps it per block
-            const int slot = (int)(((unsigned)c * 2654435761u) >> (32 - kHashLog));
-            int k = hkey[slot];
-            if (k == -1) {
-              const int prev = atomicCAS(&hkey[slot], -1, c);
-              k = prev == -1 ? c : prev;
-            }
-            if (k == c) atomicAdd(&hcnt[slot], 1);
-            else atomicAdd(&p.counts[c], 1);
-          }
-        }
+        if (!br) count_col(c);
       }
       bool head;
       const double sq = seg_sum_head(in ? v * v : 0.0, in ? j : 32 + lane, &head);

@@ -657,3 +657,40 @@ def test_combine_clusters_and_write_through_keep_every_add(name, comb, cluster, 
     A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
     assert rel(ab, A.T @ alpha / p.n) <= 1e-10
     assert np.all(np.isfinite(x)) and a.objective() < np.log(2.0)
+
+
+def _mixed_rows_problem():
+    """Short rows (mean ~6) with two 1,200-entry rows: most 32-row tiles take the ingest's
+    staged path, the two holding the long rows take the flat path."""
+    rng = np.random.Generator(np.random.PCG64(1606))
+    n, d = 2000, 3000
+    lens = rng.integers(2, 9, size=n)
+    lens[100] = lens[1500] = 1200
+    cols = [np.sort(rng.choice(d, size=L, replace=False)).astype(np.int32) for L in lens]
+    vals = [rng.standard_normal(L) for L in lens]
+    vals = [v / np.linalg.norm(v) for v in vals]
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    y = np.where(rng.standard_normal(n) >= 0, 1.0, -1.0)
+    return datagen.Problem("mixed", n, d, indptr, np.concatenate(cols), np.concatenate(vals), y, 1.0 / n)
+
+
+@gpu
+def test_ingest_mixed_tiles_staged_and_flat():
+    """A0-A1 on data whose tiles take both ingest paths: n_v, D bit-exact, L and the longest
+    row exact, f at a random x to 1e-12, and the deterministic iterate to 1e-9."""
+    m = asaga_mod()
+    p = _mixed_rows_problem()
+    a = m.Asaga.from_problem(p, gamma_of(p), deterministic=True)
+    counts, D = a.profile()
+    ref = oracle.column_counts(p)
+    assert np.array_equal(counts.astype(np.int64), ref)
+    assert np.array_equal(D, oracle.reweight(p.n, ref))
+    st = a.stats()
+    assert st["max_row"] == 1200 and st["delta_r"] == ref.max()
+    assert st["L"] == pytest.approx(oracle.lipschitz(p, p.lam), rel=1e-14)
+    x = np.random.Generator(np.random.PCG64(7)).standard_normal(p.d) * 0.1
+    assert a.objective(x) == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+    a.run(3 * p.n, SEED)
+    xg, alg, abg, _ = a.get_state()
+    r = oracle.sparse_saga(p, p.y, p.lam, gamma_of(p), SEED, 3 * p.n)
+    assert rel(xg, r.x) <= 1e-9 and rel(alg, r.alpha) <= 1e-9 and rel(abg, r.alpha_bar) <= 1e-9
