@@ -694,3 +694,92 @@ def test_ingest_mixed_tiles_staged_and_flat():
     xg, alg, abg, _ = a.get_state()
     r = oracle.sparse_saga(p, p.y, p.lam, gamma_of(p), SEED, 3 * p.n)
     assert rel(xg, r.x) <= 1e-9 and rel(alg, r.alpha) <= 1e-9 and rel(abg, r.alpha_bar) <= 1e-9
+
+
+# ---------------------------------------------------------------------- degenerate and edge cases
+@gpu
+def test_degenerate_instances_match_the_oracle():
+    """d = 1 (P10's 1-D instance, a_i = 1), rows of one entry, a feature no row uses
+    (n_v = 0 -> D_v = 0: x_v never moves), all labels +1, and n = 1: the deterministic
+    iterate within 1e-9 of the oracle's, and the unused coordinate exactly 0."""
+    m = asaga_mod()
+    cases = []
+    n = 50
+    cases.append(datagen.Problem("d1", n, 1, np.arange(n + 1, dtype=np.int64), np.zeros(n, np.int32),
+                                 np.ones(n), np.where(np.arange(n) % 3 == 0, -1.0, 1.0), 1.0 / n))
+    rng = np.random.Generator(np.random.PCG64(11))
+    cols = rng.integers(0, 7, size=n).astype(np.int32)  # one entry per row, feature 7 unused
+    cases.append(datagen.Problem("single", n, 8, np.arange(n + 1, dtype=np.int64), cols,
+                                 np.ones(n), np.ones(n), 1.0 / n))
+    cases.append(datagen.Problem("n1", 1, 3, np.array([0, 2], np.int64), np.array([0, 2], np.int32),
+                                 np.array([0.6, 0.8]), np.array([-1.0]), 1.0))
+    for p in cases:
+        g = gamma_of(p)
+        for conc in (None, 4):
+            kw = dict(deterministic=True) if conc is None else dict(concurrency=conc)
+            a = m.Asaga.from_problem(p, g, **kw)
+            a.run(7 * p.n + 3, SEED)
+            x, alpha, ab, t = a.get_state()
+            assert t == 7 * p.n + 3
+            if conc is None:
+                r = oracle.sparse_saga(p, p.y, p.lam, g, SEED, 7 * p.n + 3)
+                for got, ref in ((x, r.x), (alpha, r.alpha), (ab, r.alpha_bar)):
+                    assert rel(got, ref) <= 1e-9, (p.name, got, ref)
+            counts, D = a.profile()
+            assert np.all(x[counts == 0] == 0.0) and np.all(D[counts == 0] == 0.0)
+            assert np.all(np.isfinite(x))
+            a.close()
+
+
+@gpu
+def test_run_lengths_below_and_around_the_concurrency():
+    """Fewer updates than samples in flight, zero updates, and odd lengths: the t -> worker
+    map does not depend on the launch, so the sample stream stays bit-exact, with and
+    without combining."""
+    m = asaga_mod()
+    p = SUBSETS["c2s"]()
+    for comb in (0.0, 1e-300):
+        a = m.Asaga.from_problem(p, gamma_of(p) / 16, concurrency=1000, record_samples=True,
+                                 combine_min_freq=comb)
+        total = 0
+        for T in (0, 1, 17, 999, 1000, 1001, 4321):
+            a.run(T, SEED)
+            total += T
+        ref = np.bincount(oracle.sample_stream(SEED, 0, total, p.n), minlength=p.n)
+        assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+        assert a.get_state()[3] == total
+        a.close()
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_bench_operating_point_full_size_properties(name):
+    """c3 / c4 at BASELINE full size in the bench's launch configuration: every t processed
+    once (bit-exact histogram over all n rows), the quiescent identity, and the GPU's f at
+    its iterate equal to the oracle's f of that iterate (1e-12)."""
+    import scipy.sparse
+
+    import bench
+
+    m = asaga_mod()
+    p = datagen.make(name)
+    op = bench.OPERATING_POINT[name]
+    a = m.Asaga.from_problem(p, op["gscale"] * gamma_of(p), concurrency=op["W"], record_samples=True,
+                             **bench.asaga_options(op))
+    a.run(p.n, SEED)
+    f = a.objective()
+    ref = np.bincount(oracle.sample_stream(SEED, 0, p.n, p.n), minlength=p.n)
+    assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert f == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+    assert f < np.log(2.0)
+    a.close()
+
+
+@gpu
+def test_deterministic_c4_full_size_prefix():
+    """c4 at BASELINE full size (d = 3.2M, 2.77e8 nnz): the first 2e4 updates match the oracle."""
+    p = datagen.make("c4")
+    _det_compare(p, 20_000, [10_000, 20_000])
