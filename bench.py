@@ -4,7 +4,8 @@ A "step" = one pass of every SURVEY.md section 8(a) row over one batch of
 synthetic input:
     A0+A1  asaga_reload_device_async  validate, fold labels, n_v / D / L (non-blocking;
                                       the validation is read back by A9's call)
-    A2-A8  asaga_run_async(n)      one epoch = n ASAGA updates            1 kernel
+    A2-A8  asaga_run_async(n)      one epoch = n ASAGA updates (c2: the combine kernel,
+                                   c3/c4: the plain kernel with the hot split)   1 kernel
     A9     asaga_objective_device  f at the new iterate                   2 kernels
 value = n updates / step time (CUDA events on the context's stream, summed
 over the K timed steps, max over ranks).  512 MiB of L2 is overwritten
@@ -41,8 +42,8 @@ import datagen  # noqa: E402
 # the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
 OPERATING_POINT = {
     "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
-    # c2: every feature combined per thread block (asaga_combine_kernel), 24 workers per SM
-    "c2": dict(W=3552, gscale=0.0625, bulk=0.0, split=0.0, repl=0, comb=1e-300),
+    # c2: every feature combined per thread block (asaga_combine_kernel), 30 workers per SM
+    "c2": dict(W=4440, gscale=0.05, bulk=0.0, split=0.0, repl=0, comb=1e-300),
     # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split)
     "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.3, repl=0, comb=0.0),
     "c4": dict(W=448, gscale=0.25, bulk=0.0, split=0.3, repl=0, comb=0.0),
@@ -56,9 +57,11 @@ def asaga_options(op):
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
-    """Algorithmic HBM bytes of one update (DESIGN.md "Roofline"): the row
-    (int32 index + fp64 value + fp64 D) * s, the indptr pair, the alpha_i RMW."""
-    return 20.0 * mean_s + 16.0 + 16.0
+    """Algorithmic HBM bytes of one update (SURVEY.md 8(d), DESIGN.md section 7): the row
+    (int32 index + fp64 folded value) * s, the indptr pair, the alpha_i read-modify-write.
+    (D_v is a d-vector the method keeps resident; the plain kernel's per-entry copy of it is
+    an implementation choice, not algorithmic traffic -- it shows up in `traffic`.)"""
+    return 12.0 * mean_s + 16.0 + 16.0
 
 
 def parse():
