@@ -1095,12 +1095,19 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
   const bool solo = csize == 1;  // one block per cluster: block barriers, plain shared memory
   // The block's hot-slot tables; every thread runs this once, from its role's code, after
   // a worker has issued its prologue loads (they overlap), then the start barrier.
+  // The replica holds {x_v, q_v = D_v (abar_v + lambda x_v)}: the correction term is formed
+  // once per refresh here instead of once per entry by every worker (same expression, same
+  // rounding).
+  auto replica_of = [&](double2 xab, double Dv) {
+    return make_double2(xab.x, Dv * fma(p.lambda_, xab.x, xab.y));
+  };
   auto init_slots = [&]() {
     for (int s = threadIdx.x; s < H; s += blockDim.x) {
       const int64_t v = FULL ? s : p.hot_id[s];
-      xr[s] = ld_relaxed2(p.xa + v * p.S);
+      const double Dv = p.D[v];
+      xr[s] = replica_of(ld_relaxed2(p.xa + v * p.S), Dv);
       pend[s] = make_double2(0.0, 0.0);
-      Ds[s] = p.D[v];
+      Ds[s] = Dv;
     }
     if (threadIdx.x == 0) done = 0;
   };
@@ -1161,9 +1168,10 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           if (s < H) {
             if (solo) {  // + the adds that arrived since the exchange
               const double2 q = lds_vol2(pend + s);
-              xr[s] = make_double2(gv[b].x + q.x, gv[b].y + q.y);
+              xr[s] = replica_of(make_double2(gv[b].x + q.x, gv[b].y + q.y), Ds[s]);
             } else {
-              for (unsigned k = 0; k < csize; ++k) st_cluster_v2(mapa_shared(&xr[s], k), gv[b]);
+              const double2 r = replica_of(gv[b], Ds[s]);
+              for (unsigned k = 0; k < csize; ++k) st_cluster_v2(mapa_shared(&xr[s], k), r);
             }
           }
         }
@@ -1296,7 +1304,9 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         if (j * G >= len) break;  // group-uniform
         if (j * G + g < len) {
           dot = fma(sv[j * G + g], xb[j].x, dot);
-          qq[j] = (FULL ? Ds[sc[j * G + g]] : sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
+          // hot slot: the replica's second word is already D (abar + lambda x)
+          qq[j] = FULL || (H > 0 && ss[j * G + g] >= 0) ? xb[j].y
+                                                        : sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
         }
       }
       for (int kk = P + g; kk < len; kk += G) {  // long rows only
@@ -1305,7 +1315,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double2 v = s >= 0 ? lds_vol2(xr + s) : ld_na2(p.xa + (int64_t)c * p.S);
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
-        qs[kk - P] = (FULL ? Ds[c] : ld_nc_f64(p.dv + k)) * fma(p.lambda_, v.x, v.y);
+        qs[kk - P] = s >= 0 ? v.y : ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
       }
       dot = group_sum<G>(dot, gmask);
       // sigma~ = -1/(1+exp(m)); the correctly rounded reciprocal equals the IEEE division
