@@ -380,10 +380,12 @@ def main():
                 "peak_source": "measured by tools/microbench on B200 (profiles/microbench_b200.json)"},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "f_host": f_host},
-            # ours per step: ingest_init, ingest, profile, report, update, margin, finish,
+            # ours per step: ingest_init, ingest (for d <= 4096 its last block also runs the
+            # profile and the report; else profile + report kernels), update, margin, finish,
             # + expand_d unless every feature is combined, + hot_flag and hot_slot when
             # combining with d > 4096 (CUB's scan kernels are library, not counted)
-            "gpu_launches": (7 + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) else 1)
+            "gpu_launches": (5 + (0 if p.d <= 4096 else 2)
+                             + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) else 1)
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),
         }

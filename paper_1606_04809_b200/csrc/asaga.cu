@@ -71,6 +71,7 @@ struct asaga_ctx {
   unsigned long long* h_ing_dev = nullptr;  // ... its device address
   cudaEvent_t ev_ing = nullptr;         // recorded after the ingest's readback copies
   bool ing_pending = false;             // an asynchronous reload awaits ingest_resolve
+  bool ing_fused = false;               // the last ingest launch ran A1's finish and the report
   long long shape_key[6] = {0, 0, 0, 0, 0, 0};
   int32_t* comb_flag = nullptr;  // d scratch: hot flags, then their exclusive scan
   int32_t* comb_excl = nullptr;
@@ -463,7 +464,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   }
   TRY(dalloc(ctx, &ctx->block_loss, 2 * (size_t)ctx->obj_blocks));  // loss partials, ||x||^2 partials
   TRY(dalloc(ctx, &ctx->scal, 4));
-  TRY(dalloc(ctx, &ctx->flag, 4));
+  TRY(dalloc(ctx, &ctx->flag, 8));  // [0] non-finite, [1] max n_v, [2] hot count, [3] run guard, [4] ingest blocks
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
@@ -490,7 +491,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
 // after a host copy -- the fold is elementwise, so in place is safe).  Resets
 // the state to x = 0, alpha = 0, abar = 0, t = 0 (reading R1).
 asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
-                            const double* data_in, const double* y_in) {
+                            const double* data_in, const double* y_in, bool guard) {
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
@@ -551,9 +552,27 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
     ctx->ingest_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->sms * per_sm));
   }
   const int grid = ctx->ingest_grid;
+  // d <= 4096: the ingest's last block also runs A1's finish (D, state, Delta_r, the combine
+  // hot set) and writes the validation report -- two launches fewer per ingest
+  ip.fuse = d <= 4096 ? 1 : 0;
+  ip.xa = ctx->xa;
+  ip.S = ctx->S;
+  ip.habar = ctx->habar;
+  ip.D = ctx->D;
+  ip.comb_dmax = ctx->comb_freq > 0.0 ? 1.0 / ctx->comb_freq : 0.0;
+  ip.max_h = kCombMaxH;
+  ip.slot_of = ctx->slot_of;
+  ip.hot_id = ctx->hot_id;
+  ip.flag = ctx->flag;
+  ip.host_out = ctx->h_ing_dev;
+  ip.row_cap = ctx->row_cap;
+  ip.hot_expected = ctx->comb_freq > 0.0 ? ctx->comb_H : -1;
+  ip.guard = guard ? 1 : 0;
+  ctx->ing_fused = ip.fuse != 0;
   void* iargs[] = {&ip};
   CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
-  if (d <= 4096) {  // one block: D, state, Delta_r and the combine hot set
+  if (ip.fuse) {
+  } else if (d <= 4096) {  // one block: D, state, Delta_r and the combine hot set
     profile_small_kernel<<<1, 1024, 0, ctx->stream>>>(
         ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, (int)d, n, ctx->flag + 1,
         ctx->comb_freq > 0.0 ? 1.0 / ctx->comb_freq : 0.0, kCombMaxH,
@@ -580,9 +599,11 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
 // The validation results -> mapped pinned host memory (read by ingest_resolve now, or at
 // the next blocking call after an asynchronous reload); guard: also set the run guard.
 asaga_status enqueue_report(asaga_ctx* ctx, bool guard) {
-  ingest_report_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag, ctx->h_ing_dev, ctx->row_cap,
-                                                 ctx->comb_freq > 0.0 ? ctx->comb_H : -1, guard ? 1 : 0);
-  CK(ctx, cudaGetLastError());
+  if (!ctx->ing_fused) {  // (fused: written by the ingest's last block)
+    ingest_report_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag, ctx->h_ing_dev, ctx->row_cap,
+                                                   ctx->comb_freq > 0.0 ? ctx->comb_H : -1, guard ? 1 : 0);
+    CK(ctx, cudaGetLastError());
+  }
   CK(ctx, cudaEventRecord(ctx->ev_ing, ctx->stream));
   return ASAGA_OK;
 }
@@ -646,7 +667,7 @@ asaga_status ingest_resolve(asaga_ctx* ctx) {
 // Blocking A0-A1: enqueue, resolve, per-entry D, launch shape; the run guard opens.
 asaga_status ingest(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
                     const double* data_in, const double* y_in) {
-  TRY(ingest_enqueue(ctx, indptr_in, indices_in, data_in, y_in));
+  TRY(ingest_enqueue(ctx, indptr_in, indices_in, data_in, y_in, false));
   TRY(enqueue_report(ctx, false));
   TRY(ingest_resolve(ctx));
   TRY(enqueue_expand(ctx));
@@ -1058,7 +1079,7 @@ asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A, 
   CK(ctx, cudaSetDevice(ctx->device));
   TRY(resolve_pending(ctx));
   if (!ctx->shape_valid) return ingest(ctx, A->indptr, A->indices, A->data, y);  // no shape to keep
-  TRY(ingest_enqueue(ctx, A->indptr, A->indices, A->data, y));
+  TRY(ingest_enqueue(ctx, A->indptr, A->indices, A->data, y, true));
   TRY(enqueue_expand(ctx));
   // the run guard opens on the device iff the data is valid and fits the current launch
   TRY(enqueue_report(ctx, true));

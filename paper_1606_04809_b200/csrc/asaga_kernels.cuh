@@ -123,6 +123,21 @@ struct IngestParams {
   unsigned long long* max_len;   // longest row
   int64_t n, d, nnz;
   size_t stage_off;       // ingest_tile_kernel<true>: byte offset of the warp stages in smem
+  // fused A1 finish (d <= 4096): the last block to finish runs profile_small + the report
+  int fuse;
+  double2* xa;
+  int S;
+  double* habar;
+  double* D;
+  double comb_dmax;
+  int max_h;
+  int32_t* slot_of;
+  int32_t* hot_id;
+  int* flag;              // [1] max n_v, [2] hot count, [3] run guard, [4] finished blocks
+  unsigned long long* host_out;
+  int64_t row_cap;
+  int hot_expected;
+  int guard;
   int smem_hist;          // 1: per-block shared histogram of all d columns; 0: a per-block
                           // shared hash cache of kHashSlots columns (the popular ones claim it)
 };
@@ -161,6 +176,16 @@ __device__ __forceinline__ double seg_sum_head(double v, int key, bool* head) {
 }
 
 constexpr int kHashLog = 12, kHashSlots = 1 << kHashLog;  // ingest hash cache (32 KiB)
+
+// (defined below; the ingest's last block runs them when the A1 finish is fused)
+__device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
+                     double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
+                     int* __restrict__ max_count, double comb_dmax, int max_h,
+                     int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
+                     int* __restrict__ n_hot);
+__device__ __forceinline__ void report_body(const unsigned long long* __restrict__ scratch,
+                                            int* __restrict__ flag, unsigned long long* host_out,
+                                            int64_t row_cap, int hot_expected, int guard);
 
 // A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
 // values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
@@ -360,6 +385,21 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     for (int k = threadIdx.x; k < kHashSlots; k += blockDim.x)
       if (hkey[k] >= 0 && hcnt[k]) atomicAdd(&p.counts[hkey[k]], hcnt[k]);
   }
+  if (p.fuse) {  // the last block to finish runs A1's finish and the report (d <= 4096)
+    __shared__ int is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(&p.flag[4], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (is_last) {
+      __threadfence();
+      profile_small_body(p.counts, p.xa, p.S, p.habar, p.D, (int)p.d, p.n, p.flag + 1, p.comb_dmax, p.max_h,
+                         p.slot_of, p.hot_id, p.flag + 2);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) report_body(p.err_row, p.flag, p.host_out, p.row_cap, p.hot_expected, p.guard);
+    }
+  }
 }
 
 // A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
@@ -412,15 +452,15 @@ __global__ void ingest_init_kernel(int32_t* __restrict__ counts, int64_t d, doub
   for (int64_t i = t0; i < n; i += stride) alpha[i] = 0.0;
   if (t0 < ERR_COUNT) scratch[t0] = ~0ull;
   if (t0 < 2) scratch[ERR_COUNT + t0] = 0ull;
-  if (t0 < 4) flag[t0] = 0;
+  if (t0 < 8) flag[t0] = 0;  // [4]: the ingest's finished-block count
 }
 
 // The ingest's report, written straight into mapped pinned host memory (no copies):
 // error rows, max ||a||^2, longest row, max n_v, hot count; and the run guard for an
 // asynchronous reload (valid data that fits the launch shape), when guard != 0.
-__global__ void ingest_report_kernel(const unsigned long long* __restrict__ scratch,
-                                     int* __restrict__ flag, unsigned long long* host_out,
-                                     int64_t row_cap, int hot_expected, int guard) {
+__device__ __forceinline__ void report_body(const unsigned long long* __restrict__ scratch,
+                                            int* __restrict__ flag, unsigned long long* host_out,
+                                            int64_t row_cap, int hot_expected, int guard) {
   bool good = true;
   for (int e = 0; e < ERR_COUNT + 2; ++e) {
     host_out[e] = scratch[e];
@@ -431,12 +471,16 @@ __global__ void ingest_report_kernel(const unsigned long long* __restrict__ scra
   if (hot_expected >= 0) good = good && flag[2] == hot_expected;
   if (guard) flag[3] = good ? 1 : 0;
 }
+__global__ void ingest_report_kernel(const unsigned long long* __restrict__ scratch,
+                                     int* __restrict__ flag, unsigned long long* host_out,
+                                     int64_t row_cap, int hot_expected, int guard) {
+  report_body(scratch, flag, host_out, row_cap, hot_expected, guard);
+}
 
 // Small d (<= 1024 * 4): A1's finish and the combine hot set in ONE block -- D_v, state
 // init, Delta_r, hot flags, their exclusive scan (slots in feature order, as the CUB path
 // gives) and the slot tables -- instead of five launches.
-__global__ void __launch_bounds__(1024)
-profile_small_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
+__device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
                      double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
                      int* __restrict__ max_count, double comb_dmax, int max_h,
                      int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
@@ -500,6 +544,15 @@ profile_small_kernel(const int32_t* __restrict__ counts, double2* __restrict__ x
       slot += flag[q];
     }
   }
+}
+
+__global__ void __launch_bounds__(1024)
+profile_small_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
+                     double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
+                     int* __restrict__ max_count, double comb_dmax, int max_h,
+                     int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
+                     int* __restrict__ n_hot) {
+  profile_small_body(counts, xa, S, habar, D, d, n, max_count, comb_dmax, max_h, slot_of, hot_id, n_hot);
 }
 
 // Combining: hot features are those with 0 < D_v <= comb_dmax (p_v >= combine_min_freq).
