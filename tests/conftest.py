@@ -9,7 +9,23 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _ensure_library():
+    """Build libasaga.so in-tree if this checkout has none yet (tests import the package,
+    which refuses to load without it: there is no CPU fallback)."""
+    lib = os.path.join(ROOT, "paper_1606_04809_b200", "libasaga.so")
+    if os.path.exists(lib):
+        return
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "_asaga_build", os.path.join(ROOT, "paper_1606_04809_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+
+
 def pytest_configure(config):
+    _ensure_library()
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the C-ABI on cuda:0)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
