@@ -571,17 +571,10 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ctx->ing_fused = ip.fuse != 0;
   void* iargs[] = {&ip};
   CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
-  if (ip.fuse) {
-  } else if (d <= 4096) {  // one block: D, state, Delta_r and the combine hot set
-    profile_small_kernel<<<1, 1024, 0, ctx->stream>>>(
-        ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, (int)d, n, ctx->flag + 1,
-        ctx->comb_freq > 0.0 ? 1.0 / ctx->comb_freq : 0.0, kCombMaxH,
-        ctx->slot_of, ctx->hot_id, ctx->flag + 2);
+  if (!ip.fuse) {
+    profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->habar,
+                                                                          ctx->D, d, n, ctx->flag + 1);
     CK(ctx, cudaGetLastError());
-  } else {
-  profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, d, n,
-                                                                        ctx->flag + 1);
-  CK(ctx, cudaGetLastError());
   }
   if (ctx->comb_freq > 0.0 && d > 4096) {  // hot set of the combine kernel: p_v >= combine_min_freq
     hot_flag_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->D, d, 1.0 / ctx->comb_freq,

@@ -477,9 +477,9 @@ __global__ void ingest_report_kernel(const unsigned long long* __restrict__ scra
   report_body(scratch, flag, host_out, row_cap, hot_expected, guard);
 }
 
-// Small d (<= 1024 * 4): A1's finish and the combine hot set in ONE block -- D_v, state
-// init, Delta_r, hot flags, their exclusive scan (slots in feature order, as the CUB path
-// gives) and the slot tables -- instead of five launches.
+// Small d (<= 1024 * 4): A1's finish and the combine hot set by ONE block (the ingest's
+// last) -- D_v, state init, Delta_r, hot flags, their exclusive scan (slots in feature
+// order, as the CUB path gives) and the slot tables -- instead of five launches.
 __device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
                      double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
                      int* __restrict__ max_count, double comb_dmax, int max_h,
@@ -544,15 +544,6 @@ __device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ c
       slot += flag[q];
     }
   }
-}
-
-__global__ void __launch_bounds__(1024)
-profile_small_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa, int S,
-                     double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
-                     int* __restrict__ max_count, double comb_dmax, int max_h,
-                     int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
-                     int* __restrict__ n_hot) {
-  profile_small_body(counts, xa, S, habar, D, d, n, max_count, comb_dmax, max_h, slot_of, hot_id, n_hot);
 }
 
 // Combining: hot features are those with 0 < D_v <= comb_dmax (p_v >= combine_min_freq).
