@@ -1182,7 +1182,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
     while ((solo ? *vdone : ld_cluster_volatile_s32(done0)) < total) {
       ++passes;
       for (int s0 = (int)crank + (int)csize * lane; s0 < H; s0 += (int)csize * 32 * B) {
-        double2 gv[B];
+        double2 gv[B], gd[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           const int s = s0 + (int)csize * 32 * b;
@@ -1201,20 +1201,23 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
                 dy += exch_cluster_f64(a + 8);
               }
             }
+            // read the shared pair BEFORE sending this pass's adds (the load then does not
+            // queue behind them at the line) and count them in locally: g + d
+            gv[b] = ld_relaxed2(gp);
             if (dx != 0.0) red_add(&gp->x, dx);
             if (dy != 0.0) red_add(&gp->y, dy);
-            gv[b] = ld_relaxed2(gp);  // after this thread's own adds (same address)
+            gd[b] = make_double2(dx, dy);
           }
         }
 #pragma unroll
         for (int b = 0; b < B; ++b) {
           const int s = s0 + (int)csize * 32 * b;
           if (s < H) {
-            if (solo) {  // + the adds that arrived since the exchange
+            if (solo) {  // + this pass's adds + the adds that arrived since the exchange
               const double2 q = lds_vol2(pend + s);
-              xr[s] = replica_of(make_double2(gv[b].x + q.x, gv[b].y + q.y), Ds[s]);
+              xr[s] = replica_of(make_double2(gv[b].x + gd[b].x + q.x, gv[b].y + gd[b].y + q.y), Ds[s]);
             } else {
-              const double2 r = replica_of(gv[b], Ds[s]);
+              const double2 r = replica_of(make_double2(gv[b].x + gd[b].x, gv[b].y + gd[b].y), Ds[s]);
               for (unsigned k = 0; k < csize; ++k) st_cluster_v2(mapa_shared(&xr[s], k), r);
             }
           }
