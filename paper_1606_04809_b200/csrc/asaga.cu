@@ -576,7 +576,7 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
                                                                           ctx->D, d, n, ctx->flag + 1);
     CK(ctx, cudaGetLastError());
   }
-  if (ctx->comb_freq > 0.0 && d > 4096) {  // hot set of the combine kernel: p_v >= combine_min_freq
+  if (ctx->comb_freq > 0.0 && !ip.fuse) {  // hot set of the combine kernel: p_v >= combine_min_freq
     hot_flag_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->D, d, 1.0 / ctx->comb_freq,
                                                                           ctx->comb_flag);
     CK(ctx, cudaGetLastError());

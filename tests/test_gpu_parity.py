@@ -783,3 +783,27 @@ def test_deterministic_c4_full_size_prefix():
     """c4 at BASELINE full size (d = 3.2M, 2.77e8 nnz): the first 2e4 updates match the oracle."""
     p = datagen.make("c4")
     _det_compare(p, 20_000, [10_000, 20_000])
+
+
+@gpu
+def test_combine_hot_set_on_the_unfused_ingest_path():
+    """2048 < d <= 4096 with short rows: the ingest runs the separate profile / hot-set
+    kernels (not its fused last block); the combine kernel's hot set must still be exact
+    and every add kept (stream bit-exact, quiescent identity)."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = _mixed_rows_problem()
+    counts = oracle.column_counts(p)
+    f = 4.0 / p.n
+    a = m.Asaga.from_problem(p, gamma_of(p) / 4, concurrency=128, record_samples=True, combine_min_freq=f)
+    want = int(np.sum(counts >= f * p.n))
+    assert a.stats()["combine_hot"] == want > 0
+    T = 5 * p.n + 77
+    a.run(T, SEED)
+    ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
+    assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x))
