@@ -787,9 +787,9 @@ def test_deterministic_c4_full_size_prefix():
 
 @gpu
 def test_combine_hot_set_on_the_unfused_ingest_path():
-    """2048 < d <= 4096 with short rows: the ingest runs the separate profile / hot-set
-    kernels (not its fused last block); the combine kernel's hot set must still be exact
-    and every add kept (stream bit-exact, quiescent identity)."""
+    """A partial hot set (d = 3000, features with n_v >= 4 combined, the rest cold) on data
+    mixing short and 1,200-entry rows: the hot set is exact and every add kept (stream
+    bit-exact, quiescent identity)."""
     import scipy.sparse
 
     m = asaga_mod()
