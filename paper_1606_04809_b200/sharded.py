@@ -53,7 +53,13 @@ class ShardedObjective:
         if partial is None:
             if shard_ctx is None:
                 raise ValueError("need the shard's Asaga context (CUDA) or an explicit partial")
-            partial = lambda x, out: shard_ctx.partial_obj_grad(x, out)  # noqa: E731
+            # on torch's current stream: ordered after the broadcast / copy of x and
+            # before the all-reduce of out (the context's own stream is not).  torch's
+            # default stream has handle 0, which the C-ABI reads as "the context's stream",
+            # so it is passed as cudaStreamLegacy (0x1).
+            def partial(x, out):
+                h = torch.cuda.current_stream(self.device).cuda_stream
+                shard_ctx.partial_obj_grad(x, out, stream=h if h != 0 else 1)
         self.partial = partial
         self.out = torch.zeros(self.d + 1, dtype=torch.float64, device=self.device)
 
