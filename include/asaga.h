@@ -136,6 +136,10 @@ typedef struct {
                             every add goes straight to the shared state (red.global.add.f64),
                             so the hot lines lose their per-update loads but no add is held
                             back.  0 (default) = adds are combined per block. */
+  int combine_max_blocks; /* combining: at most this many thread blocks (replicas), >= 0; the
+                            samples in flight are packed into fewer, fuller blocks so each
+                            communication pass carries more combined adds.  0 (default) = one
+                            block per SM (per resident cluster slot). */
 } asaga_options;
 
 typedef struct {

@@ -64,6 +64,7 @@ struct asaga_ctx {
   int comb_nwb = 0;            // worker groups per block of the combine kernel
   int comb_csize = 1;          // blocks per cluster of the combine kernel
   int comb_cluster_opt = 0;    // requested cluster size (0 = 1)
+  int comb_max_blocks = 0;     // cap on the combine kernel's blocks (0 = resident capacity)
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
@@ -298,6 +299,8 @@ asaga_status comb_shape(asaga_ctx* ctx, int64_t workers, int* nwb, int* blocks, 
   }
   if (cap_clusters < 1) return fail(ctx, ASAGA_E_INVALID_ARG, "no cluster of %d blocks fits the device", C);
   int64_t cap_blocks = (int64_t)cap_clusters * C;
+  if (ctx->comb_max_blocks > 0)
+    cap_blocks = std::max<int64_t>(C, std::min<int64_t>(cap_blocks, ctx->comb_max_blocks / C * C));
   if (workers <= 0)  // auto: every resident block full of workers
     workers = cap_blocks * ((kCombBlock - 32) / ctx->lanes);
   // blocks: enough that every block has <= kCombBlock - 32 worker threads
@@ -532,16 +535,22 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.d = d;
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
+  const double mean_row = n > 0 ? (double)nnz / (double)n : 0.0;
   const size_t hist_bytes =
       ((ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t)) + 15) & ~(size_t)15;
   // short rows: warp stages (kStageCap entries per warp) when they fit next to the histogram
   const size_t stage_bytes = 32 * (size_t)kStageCap * (sizeof(double) + sizeof(int32_t));
-  const bool staged = n > 0 && (double)nnz / (double)n <= 16.0 && hist_bytes + stage_bytes <= 200 * 1024;
+  const bool staged = n > 0 && mean_row <= 16.0 && hist_bytes + stage_bytes <= 200 * 1024;
+  // long rows counted through the hash cache: one row per warp step (kIngestRows; c4 ingest
+  // kernel 3.13 -> 2.81 ms).  With a shared histogram (c3) the flat path stays ahead.
+  const bool rows = !staged && !ip.smem_hist && mean_row >= 32.0;
   const size_t hsmem = hist_bytes + (staged ? stage_bytes : 0);
   ip.stage_off = hist_bytes;
   // 32-row tiles per warp streamed flat (measured against a G-lanes-per-row variant, 77 vs
   // 69 us on c2, and a thread-per-row variant, 102 us: uncoalesced, 1.3x the DRAM bytes)
-  const void* kfn = staged ? (const void*)ingest_tile_kernel<true> : (const void*)ingest_tile_kernel<false>;
+  const void* kfn = staged ? (const void*)ingest_tile_kernel<kIngestStaged>
+                  : rows   ? (const void*)ingest_tile_kernel<kIngestRows>
+                           : (const void*)ingest_tile_kernel<kIngestFlat>;
   const int kIngestBlock = 1024;
   const int rows_per_warp = 32;
   // (the attribute is per function, shared by every context: set it on every launch)
@@ -756,6 +765,11 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
     return fail(ctx, ASAGA_E_INVALID_ARG, "combine_cluster must be in [0, 8] (got %d)", o.combine_cluster);
   }
   ctx->comb_cluster_opt = o.combine_cluster;
+  if (o.combine_max_blocks < 0) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG, "combine_max_blocks must be >= 0 (got %d)", o.combine_max_blocks);
+  }
+  ctx->comb_max_blocks = o.combine_max_blocks;
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
@@ -1020,6 +1034,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->combine_min_freq = 0.0;
   opt->combine_cluster = 0;
   opt->combine_write_through = 0;
+  opt->combine_max_blocks = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

@@ -93,6 +93,20 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
+// cp.async (LDGSTS) helpers: rows are copied global -> shared while earlier ones are
+// processed (update kernels: the next sample's row; ingest: the next row batches).
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ int ld_nc_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ld_nc_f64(const double* p) { return __ldg(p); }
 
@@ -194,10 +208,16 @@ __device__ __forceinline__ void report_body(const unsigned long long* __restrict
 // OWNER lane from shared memory (the previous index and ||a_i||^2 in registers: a few
 // instructions per entry instead of the flat path's per-chunk row search and segmented
 // reduction), and the tile is written back coalesced.  Larger tiles take the flat path.
+// ROWS (long rows, mean >= 32 entries, n_v through the hash cache): the warp walks the
+// tile row by row, 32 entries of one row per chunk: the row, label and previous column
+// are warp-uniform, so the flat path's per-chunk row search and segmented reduction (186
+// warp instructions per chunk on c4, ncu) become one warp sum per row (117 per chunk).
+enum : int { kIngestFlat = 0, kIngestStaged = 1, kIngestRows = 2 };
 constexpr int kStageCap = 512;  // entries per warp stage (int32 index + fp64 value: 6 KiB)
 
-template <bool STAGED>
+template <int MODE>
 __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
+  constexpr bool STAGED = MODE == kIngestStaged;
   extern __shared__ __align__(16) int32_t hist[];
   __shared__ double rsq[32][32];
   __shared__ double blk_max[32];
@@ -267,16 +287,17 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     const int rel = (int)((row ? lo : end) - base);
     if (STAGED && end - base <= kStageCap) {
       const int cnt = (int)(end - base);
-#pragma unroll 4
-      for (int e = lane; e < cnt; e += 32) {
-        stage_c[e] = p.indices[base + e];
-        stage_v[e] = p.data[base + e];
+      for (int e = lane; e < cnt; e += 32) {  // every copy in flight at once (cp.async)
+        cp_async4(stage_c + e, p.indices + base + e);
+        cp_async8(stage_v + e, p.data + base + e);
       }
+      cp_async_commit();
+      cp_async_wait_all();
       __syncwarp();
+      int prevc = -1;
+      double sq = 0.0;
+      bool br_any = false, bo_any = false, bv_any = false;
       if (row) {
-        int prevc = -1;
-        double sq = 0.0;
-        bool br_any = false, bo_any = false, bv_any = false;
         const int kend = rel + (int)(hi - lo);
         for (int k = rel; k < kend; ++k) {
           const int32_t c = stage_c[k];
@@ -290,6 +311,8 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
           sq = fma(v, v, sq);
           if (!br) count_col(c);
         }
+      }
+      if (row) {
         if (br_any) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
         if (bo_any) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
         if (bv_any) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
@@ -302,6 +325,60 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         p.vals[base + e] = stage_v[e];
       }
       __syncwarp();
+      continue;
+    }
+    if (MODE == kIngestRows) {
+      for (int j = 0; j < nr; ++j) {
+        const int64_t rlo = __shfl_sync(0xffffffffu, lo, j);
+        const int64_t rhi = __shfl_sync(0xffffffffu, hi, j);
+        const double bj = __shfl_sync(0xffffffffu, b, j);
+        int carry = -1;
+        double sq = 0.0;
+        bool br_any = false, bo_any = false, bv_any = false;
+        // 4 chunks (128 entries) are loaded before any is processed: loads in flight
+        // (a cp.async ring of 128-entry units, two ahead, measured slower on c4, 2.92 vs
+        // 2.81 ms: the kernel is LSU/MIO-bound, l1tex 69 %, and the ring adds a shared load)
+        for (int64_t e00 = rlo; e00 < rhi; e00 += 128) {
+          int32_t cq[4];
+          double vq[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int64_t e = e00 + 32 * qq + lane;
+            cq[qq] = e < rhi ? p.indices[e] : INT32_MAX;
+            vq[qq] = e < rhi ? p.data[e] : 0.0;
+          }
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int64_t e0 = e00 + 32 * qq;
+            if (e0 >= rhi) break;  // warp-uniform
+            const int64_t e = e0 + lane;
+            const int32_t c = cq[qq];
+            const double v = vq[qq];
+            int prev = __shfl_up_sync(0xffffffffu, c, 1);
+            if (lane == 0) prev = carry;
+            carry = __shfl_sync(0xffffffffu, c, 31);
+            if (e < rhi) {
+              const bool br = (c < 0) || ((int64_t)c >= p.d);
+              br_any |= br;
+              bo_any |= e > rlo && prev >= c;
+              bv_any |= !isfinite(v);
+              p.cols_out[e] = c;
+              p.vals[e] = bj * v;
+              sq = fma(v, v, sq);
+              if (!br) count_col(c);
+            }
+          }
+        }
+        sq = group_sum<32>(sq, 0xffffffffu);
+        const bool bad = __any_sync(0xffffffffu, br_any), bado = __any_sync(0xffffffffu, bo_any),
+                   badv = __any_sync(0xffffffffu, bv_any);
+        if (lane == j) {
+          my_max = fmax(my_max, sq);
+          if (bad) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+          if (bado) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+          if (badv) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+        }
+      }
       continue;
     }
     rsq[wib][lane] = 0.0;
@@ -628,20 +705,6 @@ struct UpdateParams {
   int split;              // hot split in use (entries with dv < 0 keep abar in habar)
   const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
 };
-
-// cp.async (LDGSTS) helpers: the next sample's row is copied global -> shared
-// while the current sample computes.  Lane g copies and later reads only its own
-// entries (k = lo + j*G + g), so no cross-lane barrier is needed.
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-               "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-               "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Shared memory per group: a P-entry {dx, dabar} source buffer for the TMA bulk
 // scatter (16-B aligned, first), 2 stages x P = NR*G row entries (fp64 value,
@@ -1090,11 +1153,6 @@ __device__ __forceinline__ void atomic_add_cluster_s32(unsigned a, int v) {
 }
 __device__ __forceinline__ double exch_shared(double* p) {
   return __longlong_as_double((long long)atomicExch(reinterpret_cast<unsigned long long*>(p), 0ull));
-}
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int G, int NR, bool FULL>

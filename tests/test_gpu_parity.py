@@ -385,7 +385,8 @@ def test_errors():
                 bulk_scatter_min_freq=0.5, hot_split_min_freq=0.5)
     assert ei.value.name == "ASAGA_E_INVALID_ARG"
     for kw in (dict(combine_min_freq=0.5, bulk_scatter_min_freq=0.5), dict(combine_min_freq=2.0),
-               dict(combine_min_freq=0.5, combine_cluster=9)):
+               dict(combine_min_freq=0.5, combine_cluster=9),
+               dict(combine_min_freq=0.5, combine_max_blocks=-1)):
         with pytest.raises(E) as ei:
             m.Asaga(ok["indptr"], ok["indices"], ok["data"], ok["y"], 2, 0.5, 1.0, **kw)
         assert ei.value.name == "ASAGA_E_INVALID_ARG", kw
@@ -694,6 +695,75 @@ def test_ingest_mixed_tiles_staged_and_flat():
     xg, alg, abg, _ = a.get_state()
     r = oracle.sparse_saga(p, p.y, p.lam, gamma_of(p), SEED, 3 * p.n)
     assert rel(xg, r.x) <= 1e-9 and rel(alg, r.alpha) <= 1e-9 and rel(abg, r.alpha_bar) <= 1e-9
+
+
+@gpu
+@pytest.mark.parametrize("L", [6, 20, 40, 150])
+def test_ingest_errors_on_every_tile_path(L):
+    """Validation on each ingest path: rows of 6 entries (staged tiles), 20
+    (flat), 40 and 150 with d > 49,152 (n_v through the hash cache, one row per warp step;
+    150 spans two 128-entry load batches).  Each defect sits in row 37 and again in row 80,
+    deep inside the row (a later chunk): the message names the FIRST bad row; a clean copy
+    ingests with exact n_v and L."""
+    m = asaga_mod()
+    rng = np.random.Generator(np.random.PCG64(37 + L))
+    n, d = 100, (400 if L < 32 else 60_000)
+    cols = [np.sort(rng.choice(d, size=L, replace=False)).astype(np.int32) for _ in range(n)]
+    vals = [rng.standard_normal(L) for _ in range(n)]
+    y = np.where(rng.standard_normal(n) >= 0, 1.0, -1.0)
+    k = L - 2  # position of the defect inside the row
+
+    def build(cols, vals, y):
+        indptr = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+        return indptr, np.concatenate(cols).astype(np.int32), np.concatenate(vals), y
+
+    ip, ix, dt, yy = build(cols, vals, y)
+    p = datagen.Problem("err", n, d, ip, ix, dt, yy, 1.0 / n)
+    a = m.Asaga(ip, ix, dt, yy, d, p.lam, 1.0)
+    counts, _ = a.profile()
+    assert np.array_equal(counts.astype(np.int64), oracle.column_counts(p))
+    assert a.stats()["L"] == pytest.approx(oracle.lipschitz(p, p.lam), rel=1e-14)
+    a.close()
+
+    def with_defect(fn):
+        c2 = [c.copy() for c in cols]
+        v2 = [v.copy() for v in vals]
+        y2 = y.copy()
+        for r in (37, 80):
+            fn(c2, v2, y2, r)
+        return build(c2, v2, y2)
+
+    def rng_bad(c, v, y, r):
+        c[r][k] = d
+
+    def order_bad(c, v, y, r):
+        c[r][k], c[r][k + 1] = c[r][k + 1], c[r][k]
+
+    def dup_bad(c, v, y, r):
+        c[r][k + 1] = c[r][k]
+
+    def neg_bad(c, v, y, r):
+        c[r][0] = -1
+
+    def nan_bad(c, v, y, r):
+        v[r][k] = np.inf
+
+    def empty_bad(c, v, y, r):
+        c[r] = c[r][:0]
+        v[r] = v[r][:0]
+
+    def label_bad(c, v, y, r):
+        y[r] = 0.5
+
+    for fn, name in ((rng_bad, "ASAGA_E_BAD_CSR"), (order_bad, "ASAGA_E_BAD_CSR"),
+                     (dup_bad, "ASAGA_E_BAD_CSR"), (neg_bad, "ASAGA_E_BAD_CSR"),
+                     (nan_bad, "ASAGA_E_BAD_CSR"), (empty_bad, "ASAGA_E_BAD_CSR"),
+                     (label_bad, "ASAGA_E_BAD_LABEL")):
+        ip2, ix2, dt2, yy2 = with_defect(fn)
+        with pytest.raises(m.AsagaError) as ei:
+            m.Asaga(ip2, ix2, dt2, yy2, d, p.lam, 1.0)
+        assert ei.value.name == name, (fn.__name__, ei.value)
+        assert "row 37" in str(ei.value), (fn.__name__, ei.value)
 
 
 # ---------------------------------------------------------------------- degenerate and edge cases
