@@ -8,8 +8,8 @@ synthetic input:
                                    c3/c4: the plain kernel with the hot split)   1 kernel
     A9     asaga_objective_device  f at the new iterate                   2 kernels
 value = n updates / step time (CUDA events on the context's stream, summed
-over the K timed steps, max over ranks).  512 MiB of L2 is overwritten
-between steps, outside the timed events.  The update kernel runs at the
+over the K timed steps, max over ranks).  512 MiB is written and read back
+between steps, outside the timed events (a cold, clean L2 at every step).  The update kernel runs at the
 workload's convergent operating point (samples in flight W, step gamma =
 scale / (3L)) chosen from the sweeps in profiles/ (DESIGN.md "Operating
 point"); the line also reports time-to-1e-6 from x = 0 at that point.
@@ -251,6 +251,14 @@ def main():
     a.set_gamma(gamma)
     stream = torch.cuda.ExternalStream(a.stream, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    flush_sink = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def l2_flush():
+        """Between steps, outside the timed events: write a buffer 4x the L2 (evicts the
+        step's data), then read it back so the lines left in L2 are clean -- the next step
+        starts cold without paying to write back the flush's own dirty lines."""
+        flush.zero_()
+        torch.sum(flush.view(torch.int64), dim=0, keepdim=True, out=flush_sink)
     f_dev = torch.zeros(1, dtype=torch.float64, device=dev)
     seed = datagen.SAMPLE_SEED
     ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -267,7 +275,7 @@ def main():
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step([ev() for _ in range(4)])
-            flush.zero_()
+            l2_flush()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -278,7 +286,7 @@ def main():
                 evs = [ev() for _ in range(4)]
                 step(evs)
                 all_evs.append(evs)
-                flush.zero_()
+                l2_flush()
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -309,7 +317,7 @@ def main():
         dt = (time.perf_counter() - t0) * 1e3
         if k >= args.warmup:
             e2e_ms.append(dt)
-        flush.zero_()
+        l2_flush()
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -361,7 +369,7 @@ def main():
                        "bulk_scatter_min_freq": bulk, "hot_split_min_freq": op["split"],
                        "smem_replica_refresh": op["repl"], "combine_min_freq": op["comb"],
                        "combine_hot_features": st["combine_hot"],
-                       "l2_flush": "512 MiB write between steps (outside the timed events)",
+                       "l2_flush": "512 MiB write + read-back between steps (outside the timed events): every step starts with a cold, clean L2",
                        "parallelism": f"{world} independent lambda-sweep instances" if world > 1 else "1 GPU"},
             "breakdown_ms": {"ingest_A0_A1": float(np.mean(ing_ms)), "updates_A2_A8": float(np.mean(upd_ms)),
                              "objective_A9": float(np.mean(obj_ms))},

@@ -172,8 +172,7 @@ typedef struct {
 ASAGA_API void asaga_options_default(asaga_options* opt);
 
 /* Copy a HOST CSR matrix and labels y[n] (each +-1) to the device, validate it
- * (see ASAGA_E_BAD_CSR / _BAD_LABEL), fold labels into the values
- * (a~_i = b_i a_i, exact), and run the column-frequency pass: n_v, D_v = n/n_v
+ * (see ASAGA_E_BAD_CSR / _BAD_LABEL), and run the column-frequency pass: n_v, D_v = n/n_v
  * (0 when n_v = 0), Delta_r, L (Section 2).  State
  * starts at x = 0, alpha = 0, abar = 0, t = 0 (reading R1).  On success *out
  * owns all device memory; on failure *out = NULL. */
@@ -181,15 +180,19 @@ ASAGA_API asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, cons
                         double lambda, double gamma, const asaga_options* opt);
 
 /* As asaga_init, but A's three arrays and y are DEVICE pointers (e.g. torch
- * tensors); they are copied device-to-device and may be freed afterwards.
- * Validation runs on the device. */
+ * tensors).  They are BORROWED, not copied: the context reads them (never writes)
+ * until the next reload or asaga_destroy, so the caller keeps them allocated and
+ * unchanged until then.  Validation runs on the device.  (The labels are applied per
+ * sample and per row in the kernels -- a~_i = b_i a_i is never materialised -- so an
+ * ingest moves the matrix once, read-only.) */
 ASAGA_API asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* A_dev,
                                const double* y_dev, double lambda, double gamma,
                                const asaga_options* opt);
 
 /* Re-ingest a new matrix of the SAME shape (n, d, nnz) into an existing
- * context, reusing its device memory: HOST arrays (asaga_reload) or DEVICE
- * arrays (asaga_reload_device).  Runs A0-A1 again and resets the state to
+ * context, reusing its device memory: HOST arrays (asaga_reload; copied into the
+ * context's own device arrays) or DEVICE arrays (asaga_reload_device; borrowed as
+ * in asaga_init_device, in place of the previous ones).  Runs A0-A1 again and resets the state to
  * x = 0, alpha = 0, abar = 0, t = 0.  Errors as asaga_init; a different shape
  * gives ASAGA_E_INVALID_ARG.  Blocking (the validation result is read back). */
 ASAGA_API asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y);
@@ -197,7 +200,8 @@ ASAGA_API asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view*
                                            const double* y_dev);
 
 /* As asaga_reload_device, but NON-blocking: A0-A1 are enqueued on the context's stream
- * and the call returns at once (x = 0, alpha = 0, abar = 0, t = 0 as above).  The
+ * and the call returns at once (x = 0, alpha = 0, abar = 0, t = 0 as above); the
+ * arrays are borrowed as in asaga_init_device.  The
  * validation is read back by the next BLOCKING call on the context (asaga_run,
  * asaga_objective[_device], asaga_get_state, asaga_stats, ...), which returns its error
  * (ASAGA_E_BAD_CSR / _BAD_LABEL with the row, as asaga_reload would).  Until then every

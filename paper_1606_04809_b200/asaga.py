@@ -205,7 +205,8 @@ class Asaga:
         self._h = None
         _check(st, None)
         self._h = h
-        self._keep = None
+        # device arrays are borrowed by the context (read until the next reload / close)
+        self._keep = (indptr, indices, data, y) if device_inputs else None
         self.n, self.d, self.nnz = n, int(d), nnz
         self.lam = float(lam)
         self.device = device
@@ -243,14 +244,15 @@ class Asaga:
                        _ptr(indices), _ptr(data))
         fn = _lib.asaga_reload_device if dev else _lib.asaga_reload
         _check(fn(self._h, ctypes.byref(view), _ptr(y)), self._h)
+        self._keep = (indptr, indices, data, y) if dev else None  # borrowed device arrays
 
     def reload_async(self, indptr, indices, data, y) -> None:
-        """Non-blocking device re-ingest (CUDA tensors, which must stay alive until the
-        next blocking call); validation is reported by that call."""
+        """Non-blocking device re-ingest (CUDA tensors, borrowed by the context until the
+        next reload / close); validation is reported by the next blocking call."""
         assert _is_cuda(indptr), "reload_async takes device (CUDA) arrays"
         view = CsrView(int(indptr.shape[0]) - 1, self.d, int(indices.shape[0]), _ptr(indptr),
                        _ptr(indices), _ptr(data))
-        self._keep_async = (indptr, indices, data, y)
+        self._keep = (indptr, indices, data, y)
         _check(_lib.asaga_reload_device_async(self._h, ctypes.byref(view), _ptr(y)), self._h)
 
     def run(self, n_updates: int, seed: int) -> None:

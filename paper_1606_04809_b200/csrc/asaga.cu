@@ -46,11 +46,18 @@ struct asaga_ctx {
   int deterministic = 0, atomic_mode = 1, record = 0;
   int64_t concurrency_opt = 0;
   int lanes_opt = 0;
-  // device data
-  int64_t* rowptr = nullptr;
-  int32_t* cols = nullptr;
-  double* vals = nullptr;  // folded a~ = b a
-  double* y = nullptr;
+  // device data.  The matrix the kernels read is never copied on the device: the caller's
+  // device arrays (borrowed by asaga_init_device / asaga_reload_device*: they must outlive
+  // their use) or the context's own copies of host arrays (own_*, allocated on first use).
+  // Values are the caller's a_ik; the label b_i is applied per sample / row (exact).
+  const int64_t* rowptr = nullptr;
+  const int32_t* cols = nullptr;
+  const double* vals = nullptr;
+  const double* y = nullptr;
+  int64_t* own_rowptr = nullptr;
+  int32_t* own_cols = nullptr;
+  double* own_vals = nullptr;
+  double* own_y = nullptr;
   double2* xa = nullptr;   // {x_v, abar_v} pairs at xa[v * S]
   int S = 1;               // pair stride
   double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
@@ -261,7 +268,7 @@ size_t comb_group_bytes(const asaga_ctx* ctx) {  // CombSmem<G, NR, FULL>::bytes
   const bool full = ctx->comb_H == ctx->d;
   const size_t P = (size_t)ctx->nr * ctx->lanes;
   const size_t alpha_off = full ? P * (sizeof(double) + sizeof(int32_t)) : P * (2 * sizeof(double) + 2 * sizeof(int32_t));
-  const size_t stage = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
+  const size_t stage = (alpha_off + 2 * sizeof(double) + 15) & ~(size_t)15;  // + alpha_i, b_i
   // KS = 3 row stages + a bounds ring of 2 KS 32-byte slots + overflow q slots
   return (3 * stage + 6 * 32 + (size_t)ctx->overflow * sizeof(double) + 15) & ~(size_t)15;
 }
@@ -375,8 +382,8 @@ asaga_status configure_update(asaga_ctx* ctx) {
   // (GroupSmem in asaga_kernels.cuh)
   // (GroupSmem: bulk-scatter source buffer + 2 row stages + overflow q slots)
   const size_t group_bytes = (size_t)nr * lanes * 2 * sizeof(double) +
-                             2 * (size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
-                             (size_t)ctx->overflow * sizeof(double);
+                             2 * ((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) + 16) +
+                             (size_t)ctx->overflow * sizeof(double);  // (+16: b_i per stage)
   ctx->group_bytes = group_bytes;
   if (use_combine(ctx)) {
     int64_t workers = ctx->concurrency_opt > 0 ? ctx->concurrency_opt : 0;
@@ -435,10 +442,6 @@ asaga_status configure_update(asaga_ctx* ctx) {
 // Device buffers of a context (sizes fixed by n, d, nnz).
 asaga_status alloc_state(asaga_ctx* ctx) {
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
-  TRY(dalloc(ctx, &ctx->rowptr, n + 1));
-  TRY(dalloc(ctx, &ctx->cols, nnz));
-  TRY(dalloc(ctx, &ctx->y, n));
-  TRY(dalloc(ctx, &ctx->vals, nnz));
   // Small d (every feature hot, e.g. c2's d = 54): give every feature its own
   // 1 KiB block so hot features spread over L2 slices (2.2x at 1024 in flight,
   // profiles/r01_update_kernel.md); larger d keeps pairs dense (S = 8 measured no gain on c3).
@@ -523,10 +526,11 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.indices = indices_in;
   ip.data = data_in;
   ip.y = y_in;
-  ip.rowptr_out = ctx->rowptr;
-  ip.cols_out = ctx->cols;
-  ip.y_out = ctx->y;
-  ip.vals = ctx->vals;
+  // from here on the kernels read these arrays (no device-side copy)
+  ctx->rowptr = indptr_in;
+  ctx->cols = indices_in;
+  ctx->vals = data_in;
+  ctx->y = y_in;
   ip.counts = ctx->counts;
   ip.err_row = scratch;
   ip.max_sq = scratch + ERR_COUNT;
@@ -851,7 +855,7 @@ asaga_status ensure_csc(asaga_ctx* ctx) {
   if ((st = dalloc(ctx, &ctx->csc_rows, nnz)) != ASAGA_OK) { cleanup(); return st; }
   if ((st = dalloc(ctx, &ctx->csc_vals, nnz)) != ASAGA_OK) { cleanup(); return st; }
   row_of_kernel<<<grid_for(ctx, n * 32, kBlock), kBlock, 0, s>>>(ctx->rowptr, n, row_of);
-  csc_gather_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, s>>>(perm_out, row_of, ctx->vals, nnz,
+  csc_gather_kernel<<<grid_for(ctx, nnz, kBlock), kBlock, 0, s>>>(perm_out, row_of, ctx->vals, ctx->y, nnz,
                                                                     ctx->csc_rows, ctx->csc_vals);
   CKC(cudaGetLastError());
   // fixed segments of <= kColSeg entries per column (deterministic summation order)
@@ -885,16 +889,16 @@ asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, doub
   // short rows: G lanes per row (G ~ mean/3); long rows: 32-row tiles streamed flat
   const double mean = (double)ctx->nnz / (double)ctx->n;
   if (mean <= 16.0)
-    margin_thread_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
+    margin_thread_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
                                                             ctx->n, sig, ctx->block_loss, ctx->d);
   else if (mean <= 24.0)
-    margin_rows_kernel<8, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
+    margin_rows_kernel<8, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
                                                                  ctx->n, sig, ctx->block_loss, ctx->d);
   else if (ctx->margin_tiles)
-    margin_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs, ctx->n, sig,
+    margin_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs, ctx->n, sig,
                                                      ctx->block_loss, ctx->d);
   else
-    margin_rows_kernel<32, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, x_dev, xs,
+    margin_rows_kernel<32, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
                                                                   ctx->n, sig, ctx->block_loss, ctx->d);
   CK(ctx, cudaGetLastError());
   finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, xs, ctx->d,
@@ -937,6 +941,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.rowptr = ctx->rowptr;
   p.cols = ctx->cols;
   p.vals = ctx->vals;
+  p.y = ctx->y;
   p.dv = ctx->dv;
   p.D = ctx->D;
   p.xa = ctx->xa;
@@ -1074,24 +1079,29 @@ asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double*
   if (A->indptr[0] != 0 || A->indptr[A->n] != A->nnz)
     return fail(ctx, ASAGA_E_BAD_CSR, "indptr[0] must be 0 and indptr[n] must be nnz (got %lld and %lld, nnz=%lld)",
                 (long long)A->indptr[0], (long long)A->indptr[A->n], (long long)A->nnz);
-  // host -> device: the host/device boundary.  Values land in ctx->vals and are
-  // folded in place by the ingest kernel.
-  CK(ctx, cudaMemcpyAsync(ctx->rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1),
+  // host -> device: the host/device boundary, into the context's own arrays
+  if (!ctx->own_rowptr) {
+    TRY(dalloc(ctx, &ctx->own_rowptr, ctx->n + 1));
+    TRY(dalloc(ctx, &ctx->own_cols, ctx->nnz));
+    TRY(dalloc(ctx, &ctx->own_vals, ctx->nnz));
+    TRY(dalloc(ctx, &ctx->own_y, ctx->n));
+  }
+  CK(ctx, cudaMemcpyAsync(ctx->own_rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1),
                           cudaMemcpyHostToDevice, ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyHostToDevice,
+  CK(ctx, cudaMemcpyAsync(ctx->own_cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyHostToDevice,
                           ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->vals, A->data, sizeof(double) * ctx->nnz, cudaMemcpyHostToDevice,
+  CK(ctx, cudaMemcpyAsync(ctx->own_vals, A->data, sizeof(double) * ctx->nnz, cudaMemcpyHostToDevice,
                           ctx->stream));
-  CK(ctx, cudaMemcpyAsync(ctx->y, y, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
-  return ingest(ctx, ctx->rowptr, ctx->cols, ctx->vals, ctx->y);
+  CK(ctx, cudaMemcpyAsync(ctx->own_y, y, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+  return ingest(ctx, ctx->own_rowptr, ctx->own_cols, ctx->own_vals, ctx->own_y);
 }
 
 asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
   TRY(check_same_shape(ctx, A, y));
   CK(ctx, cudaSetDevice(ctx->device));
   TRY(resolve_pending(ctx));  // an asynchronous reload's validation
-  // the ingest pass itself checks indptr[0] = 0, indptr[n] = nnz (no extra round trip) and
-  // copies rowptr / cols / y into the context (one read each)
+  // the ingest pass itself checks indptr[0] = 0, indptr[n] = nnz (no extra round trip);
+  // the context then reads the caller's arrays (borrowed until the next reload / destroy)
   return ingest(ctx, A->indptr, A->indices, A->data, y);
 }
 

@@ -123,14 +123,12 @@ enum : int { ERR_ENDS = 0, ERR_ROW_BOUNDS, ERR_EMPTY_ROW, ERR_INDEX_RANGE, ERR_I
              ERR_NONFINITE, ERR_LABEL, ERR_COUNT };
 
 struct IngestParams {
-  const int64_t* indptr;  // n+1   (caller's array, or the context's after a host copy)
+  // the matrix is read, never written: the context keeps these arrays (the caller's
+  // device arrays, or its own after a host copy) and applies b_i per sample / row
+  const int64_t* indptr;  // n+1
   const int32_t* indices; // nnz
-  const double* data;     // nnz (unfolded)
+  const double* data;     // nnz
   const double* y;        // n
-  int64_t* rowptr_out;    // the context's own copies (may alias the inputs: in place)
-  int32_t* cols_out;
-  double* y_out;
-  double* vals;           // out: folded values b_i a_ik (may alias data)
   int32_t* counts;        // out (pre-zeroed): n_v
   unsigned long long* err_row;   // [ERR_COUNT], pre-set to ULLONG_MAX; atomicMin(row)
   unsigned long long* max_sq;    // bits of max_i ||a_i||^2 (>= 0 doubles order as u64)
@@ -269,12 +267,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     const int64_t lo = row ? p.indptr[i] : 0;
     const int64_t hi = row ? p.indptr[i + 1] : 0;
     const double b = row ? p.y[i] : 1.0;
-    if (row) {
-      p.rowptr_out[i] = lo;
-      if (i == p.n - 1) p.rowptr_out[p.n] = hi;
-      p.y_out[i] = b;
-      if (b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
-    }
+    if (row && b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
     // bounds: every row inside [0, nnz], monotone, contiguous with the next row
     const int64_t next_lo = __shfl_down_sync(0xffffffffu, lo, 1);
     const bool bad_b = row && (lo < 0 || hi > p.nnz || hi < lo || (lane + 1 < nr && next_lo != hi));
@@ -287,51 +280,58 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     const int rel = (int)((row ? lo : end) - base);
     if (STAGED && end - base <= kStageCap) {
       const int cnt = (int)(end - base);
-      for (int e = lane; e < cnt; e += 32) {  // every copy in flight at once (cp.async)
-        cp_async4(stage_c + e, p.indices + base + e);
-        cp_async8(stage_v + e, p.data + base + e);
+      {
+        const int32_t* gi = p.indices + base;
+        const double* gv = p.data + base;
+        for (int e = lane; e < cnt; e += 32) {  // every copy in flight at once (cp.async)
+          cp_async4(stage_c + e, gi + e);
+          cp_async8(stage_v + e, gv + e);
+        }
       }
       cp_async_commit();
       cp_async_wait_all();
       __syncwarp();
-      int prevc = -1;
-      double sq = 0.0;
-      bool br_any = false, bo_any = false, bv_any = false;
       if (row) {
+        // one "defect" flag per row in the hot loop (range or order; a non-finite value
+        // shows in sq), classified by a rescan only when set
+        const unsigned ud = (unsigned)(p.d < (int64_t)INT32_MAX + 1 ? p.d : (int64_t)INT32_MAX + 1);
+        int prevc = -1;
+        double sq = 0.0;
+        bool bad = false;
         const int kend = rel + (int)(hi - lo);
         for (int k = rel; k < kend; ++k) {
           const int32_t c = stage_c[k];
           const double v = stage_v[k];
-          const bool br = (c < 0) || ((int64_t)c >= p.d);
-          br_any |= br;
-          bo_any |= prevc >= c;
-          bv_any |= !isfinite(v);
+          const bool br = (unsigned)c >= ud;
+          bad |= br | (prevc >= c);
           prevc = c;
-          stage_v[k] = b * v;
           sq = fma(v, v, sq);
           if (!br) count_col(c);
         }
-      }
-      if (row) {
-        if (br_any) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
-        if (bo_any) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
-        if (bv_any) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+        if (bad || !isfinite(sq)) {
+          bool br_any = false, bo_any = false, bv_any = false;
+          prevc = -1;
+          for (int k = rel; k < kend; ++k) {
+            const int32_t c = stage_c[k];
+            const double v = stage_v[k];
+            br_any |= (c < 0) || ((int64_t)c >= p.d);
+            bo_any |= prevc >= c;
+            bv_any |= !isfinite(v);
+            prevc = c;
+          }
+          if (br_any) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+          if (bo_any) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+          if (bv_any) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+        }
         my_max = fmax(my_max, sq);
       }
-      __syncwarp();
-#pragma unroll 4
-      for (int e = lane; e < cnt; e += 32) {
-        p.cols_out[base + e] = stage_c[e];
-        p.vals[base + e] = stage_v[e];
-      }
-      __syncwarp();
+      __syncwarp();  // the stage is refilled by the next tile
       continue;
     }
     if (MODE == kIngestRows) {
       for (int j = 0; j < nr; ++j) {
         const int64_t rlo = __shfl_sync(0xffffffffu, lo, j);
         const int64_t rhi = __shfl_sync(0xffffffffu, hi, j);
-        const double bj = __shfl_sync(0xffffffffu, b, j);
         int carry = -1;
         double sq = 0.0;
         bool br_any = false, bo_any = false, bv_any = false;
@@ -362,8 +362,6 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
               br_any |= br;
               bo_any |= e > rlo && prev >= c;
               bv_any |= !isfinite(v);
-              p.cols_out[e] = c;
-              p.vals[e] = bj * v;
               sq = fma(v, v, sq);
               if (!br) count_col(c);
             }
@@ -407,7 +405,6 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
       const int off = (int)(e - base);
       const int j = tile_row_of(off, rel, nr);
       const int rs = __shfl_sync(0xffffffffu, rel, j);
-      const double bj = __shfl_sync(0xffffffffu, b, j);
       int prev = __shfl_up_sync(0xffffffffu, c, 1);
       if (lane == 0) prev = carry;
       carry = __shfl_sync(0xffffffffu, c, 31);
@@ -419,8 +416,6 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         if (bo) first_bad_order = min(first_bad_order, j);
         if (bv) first_bad_val = min(first_bad_val, j);
         bad_range |= br; bad_order |= bo; bad_val |= bv;
-        p.cols_out[e] = c;
-        p.vals[e] = bj * v;
         if (!br) count_col(c);
       }
       bool head;
@@ -670,7 +665,8 @@ __global__ void hot_slot_kernel(const int32_t* __restrict__ flag, const int32_t*
 struct UpdateParams {
   const int64_t* rowptr;
   const int32_t* cols;
-  const double* vals;   // folded a~
+  const double* vals;   // a (the caller's values; the label is applied per sample)
+  const double* y;      // b_i in {-1, +1}
   const double* dv;     // D_{c_k} per stored entry (not read by the FULL combine kernel)
   const double* D;      // D_v (combine kernel: the hot features' table)
   double2* xa;          // {x_v, abar_v} at xa[v * S]
@@ -713,7 +709,9 @@ template <int G, int NR>
 struct GroupSmem {
   static constexpr int P = NR * G;
   static constexpr size_t delta_bytes = (size_t)P * 2 * sizeof(double);
-  static constexpr size_t stage_bytes = (size_t)P * (2 * sizeof(double) + sizeof(int32_t));
+  // a stage: P values, P D's, P columns, then b_i (16-B slot; P * 20 is a multiple of 16)
+  static constexpr size_t stage_bytes = (size_t)P * (2 * sizeof(double) + sizeof(int32_t)) + 16;
+  static constexpr size_t label_off = (size_t)P * (2 * sizeof(double) + sizeof(int32_t));
   static __host__ __device__ size_t bytes(int overflow) {
     return delta_bytes + 2 * stage_bytes + (size_t)overflow * sizeof(double);
   }
@@ -737,11 +735,13 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 template <int G, int NR>
 __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, const int32_t* cols,
-                                               const double* vals, const double* dv, int64_t lo,
-                                               int64_t hi, int g) {
+                                               const double* vals, const double* dv, const double* b_i,
+                                               int64_t lo, int64_t hi, int g) {
   constexpr int P = NR * G;
   double* sv = reinterpret_cast<double*>(base + GroupSmem<G, NR>::delta_bytes +
                                          stage * GroupSmem<G, NR>::stage_bytes);
+  if (g == 0)
+    cp_async8(reinterpret_cast<unsigned char*>(sv) + GroupSmem<G, NR>::label_off, b_i);
   double* sd = sv + P;
   int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
   const int len = (int)(hi - lo);
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   int64_t i = sample_of(0);
   int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
   int stage = 0;
-  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, lo, hi, g);
+  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, p.y + i, lo, hi, g);
   int64_t in1 = 0, lo1 = 0, hi1 = 0, in2 = 0;
   in1 = sample_of(1);
   in2 = sample_of(2);
@@ -861,6 +861,10 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
                                                        stage * GroupSmem<G, NR>::stage_bytes);
     const double* sd = sv + P;
     const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
+    // b_i came with the row (carrying it in registers next to the row bounds measured 9 %
+    // slower on c3; a plain load next to alpha_i's, 2 %)
+    const double yb = *reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(sv) +
+                                                       GroupSmem<G, NR>::label_off);
     // gathers of x^, abar^ and D for every resident chunk are issued before any use
     double qq[NR];
     double2 xb[NR];
@@ -895,7 +899,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #else
     constexpr bool copy_late = false;
 #endif
-    if (has1 && !copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
+    if (has1 && !copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g);
     int64_t lo2 = 0, hi2 = 0;
     if (has2) {
       lo2 = __ldg(&p.rowptr[in2]);
@@ -921,16 +925,17 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       dot = fma(a, v.x, dot);
       qs[k - lo - P] = fabs(Dv) * fma(p.lambda_, v.x, v.y);
     }
-    if (has1 && copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, lo1, hi1, g);
+    if (has1 && copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g);
     TMARK(1);
     // ---- scalar derivative (folded logistic) and memory difference
-    dot = group_sum<G>(dot, gmask);
+    dot = group_sum<G>(dot, gmask) * yb;  // folded margin b_i a_i . x^ (exact: b = +-1)
 #ifdef ASAGA_TIMING
     const double sig = (p.debug_mode & 2) ? -0.5 + 0.0 * dot : -1.0 / (1.0 + exp(dot));
 #else
     const double sig = -__drcp_rn(1.0 + exp(dot));  // correctly rounded: == -1.0 / (1 + e)
 #endif
     const double da = sig - ai;
+    const double db = da * yb;  // dalpha a~_k = (dalpha b_i) a_k, exact
     const double ngam = -p.gamma;
     TMARK(2);
 #ifdef ASAGA_TIMING
@@ -947,17 +952,17 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       if (j * G + g < len) {
         const int c = sc[j * G + g];
         const double a = sv[j * G + g];
-        const double u = fma(da, a, qq[j]);
+        const double u = fma(db, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
         double* abv = (p.split && sd[j * G + g] < 0.0) ? p.habar + c : xv + 1;  // hot split
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
-          dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : da * a * p.inv_n);
+          dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : db * a * p.inv_n);
         } else if (MODE >= 1) {
           red_add(xv, ngam * u);
-          if (!p.frozen) red_add(abv, da * a * p.inv_n);
+          if (!p.frozen) red_add(abv, db * a * p.inv_n);
         } else {
           st_cg(xv, ld_cg(xv) + ngam * u);
-          if (!p.frozen) st_cg(abv, ld_cg(abv) + da * a * p.inv_n);
+          if (!p.frozen) st_cg(abv, ld_cg(abv) + db * a * p.inv_n);
         }
       }
     }
@@ -977,15 +982,15 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
-      const double u = fma(da, a, qs[k - lo - P]);
+      const double u = fma(db, a, qs[k - lo - P]);
       double* xv = &p.xa[(int64_t)c * p.S].x;
       double* abv = ld_nc_f64(p.dv + k) < 0.0 ? p.habar + c : xv + 1;  // hot split
       if (ATOMIC) {
         red_add(xv, ngam * u);
-        if (!p.frozen) red_add(abv, da * a * p.inv_n);
+        if (!p.frozen) red_add(abv, db * a * p.inv_n);
       } else {
         st_cg(xv, ld_cg(xv) + ngam * u);
-        if (!p.frozen) st_cg(abv, ld_cg(abv) + da * a * p.inv_n);
+        if (!p.frozen) st_cg(abv, ld_cg(abv) + db * a * p.inv_n);
       }
     }
 #ifdef ASAGA_TIMING
@@ -1088,7 +1093,7 @@ struct CombSmem {
   // (FULL: every feature has a slot and D_v comes from the block's table, not the stream)
   static constexpr size_t alpha_off = FULL ? (size_t)P * (sizeof(double) + sizeof(int32_t))
                                            : (size_t)P * (2 * sizeof(double) + 2 * sizeof(int32_t));
-  static constexpr size_t stage_bytes = (alpha_off + sizeof(double) + 15) & ~(size_t)15;
+  static constexpr size_t stage_bytes = (alpha_off + 2 * sizeof(double) + 15) & ~(size_t)15;  // + alpha_i, b_i
   // bounds ring: {lo, hi, i} of samples fetched 2 KS ahead (cp.async, no register waits)
   static constexpr int NB = 2 * KS;
   static constexpr size_t ring_off = KS * stage_bytes;
@@ -1158,11 +1163,14 @@ __device__ __forceinline__ double exch_shared(double* p) {
 template <int G, int NR, bool FULL>
 __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage, const int32_t* cols,
                                                  const int32_t* eslot, const double* vals,
-                                                 const double* dv, const double* alpha_i, int64_t lo,
-                                                 int64_t hi, int g) {
+                                                 const double* dv, const double* alpha_i, const double* b_i,
+                                                 int64_t lo, int64_t hi, int g) {
   constexpr int P = NR * G;
   unsigned char* sb = base + stage * CombSmem<G, NR, FULL>::stage_bytes;
-  if (g == 0) cp_async8(sb + CombSmem<G, NR, FULL>::alpha_off, alpha_i);
+  if (g == 0) {
+    cp_async8(sb + CombSmem<G, NR, FULL>::alpha_off, alpha_i);
+    cp_async8(sb + CombSmem<G, NR, FULL>::alpha_off + sizeof(double), b_i);
+  }
   double* sv = reinterpret_cast<double*>(sb);
   double* sd = sv + P;  // !FULL only
   int32_t* sc = reinterpret_cast<int32_t*>(sv + (FULL ? P : 2 * P));
@@ -1363,7 +1371,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         fetch_bounds((uint64_t)(k + KS), k + KS);
         if (t_first + (uint64_t)k * W < tend) {
           if (g == 0) { ring[4 * k] = plo[k]; ring[4 * k + 1] = phi[k]; ring[4 * k + 2] = pis[k]; }
-          issue_row_copy_c<G, NR, FULL>(gbase, k, p.cols, p.eslot, p.vals, p.dv, p.alpha + pis[k], plo[k],
+          issue_row_copy_c<G, NR, FULL>(gbase, k, p.cols, p.eslot, p.vals, p.dv, p.alpha + pis[k], p.y + pis[k], plo[k],
                                         phi[k], g);
         } else {
           cp_async_commit();
@@ -1392,6 +1400,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       const int32_t* sc = reinterpret_cast<const int32_t*>(sv + (FULL ? P : 2 * P));
       const int32_t* ss = sc + P;
       const double ai = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off);
+      const double bi = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off + 8);
       double2 xb[NR];
       double qq[NR];
 #pragma unroll
@@ -1422,9 +1431,10 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
         qs[kk - P] = s >= 0 ? v.y : ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
       }
-      dot = group_sum<G>(dot, gmask);
+      dot = group_sum<G>(dot, gmask) * bi;  // folded margin (exact: b = +-1)
       // sigma~ = -1/(1+exp(m)); the correctly rounded reciprocal equals the IEEE division
       const double da = -__drcp_rn(1.0 + exp(dot)) - ai;
+      const double db = da * bi;  // dalpha a~_k = (dalpha b_i) a_k, exact
       const double ngam = -p.gamma;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
@@ -1433,8 +1443,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           const int c = sc[j * G + g];
           const int s = FULL ? c : (H > 0 ? ss[j * G + g] : -1);
           const double a = sv[j * G + g];
-          double dx = ngam * fma(da, a, qq[j]);
-          double dy = p.frozen ? 0.0 : da * a * p.inv_n;
+          double dx = ngam * fma(db, a, qq[j]);
+          double dy = p.frozen ? 0.0 : db * a * p.inv_n;
           if (s >= 0 && !p.wt) {
             // groups of this warp that add to the same hot slot in this chunk merge their
             // adds first (xor partners; only lanes converged here take part)
@@ -1460,7 +1470,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
           } else {
             double* xv = &p.xa[(int64_t)c * p.S].x;
             red_add(xv, dx);
-            if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+            if (!p.frozen) red_add(xv + 1, db * a * p.inv_n);
           }
         }
       }
@@ -1469,14 +1479,14 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int c = ld_nc_i32(p.cols + k);
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
         const double a = ld_nc_f64(p.vals + k);
-        const double dx = ngam * fma(da, a, qs[kk - P]);
+        const double dx = ngam * fma(db, a, qs[kk - P]);
         if (s >= 0 && !p.wt) {
           atomicAdd(&pend[s].x, dx);
-          if (!p.frozen) atomicAdd(&pend[s].y, da * a * p.inv_n);
+          if (!p.frozen) atomicAdd(&pend[s].y, db * a * p.inv_n);
         } else {
           double* xv = &p.xa[(int64_t)c * p.S].x;
           red_add(xv, dx);
-          if (!p.frozen) red_add(xv + 1, da * a * p.inv_n);
+          if (!p.frozen) red_add(xv + 1, db * a * p.inv_n);
         }
       }
       if (g == 0) {
@@ -1508,8 +1518,8 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         const int64_t* nb = ring + 4 * rf;
         const int64_t nlo = nb[0], nhi = nb[1], ni = nb[2];
         fetch_bounds((uint64_t)(mf + KS), rs);  // slot of m + 2KS == slot of m
-        issue_row_copy_c<G, NR, FULL>(gbase, stage, p.cols, p.eslot, p.vals, p.dv, p.alpha + ni, nlo,
-                                      nhi, g);
+        issue_row_copy_c<G, NR, FULL>(gbase, stage, p.cols, p.eslot, p.vals, p.dv, p.alpha + ni, p.y + ni,
+                                      nlo, nhi, g);
       } else {
         cp_async_commit();
       }
@@ -1568,7 +1578,8 @@ __device__ __forceinline__ void block_partials(double acc, const double* __restr
 // A9 margins for short rows (mean <= 16): one thread per row (see ingest_thread_kernel).
 __global__ void __launch_bounds__(256)
 margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-                     const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
+                     const double* __restrict__ vals, const double* __restrict__ y,
+                     const double* __restrict__ x, int xs, int64_t n,
                      double* __restrict__ sig, double* __restrict__ block_out, int64_t d) {
   __shared__ double wl[8], wq[8];
   double acc = 0.0;
@@ -1577,6 +1588,7 @@ margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restri
     double m = 0.0;
 #pragma unroll 4
     for (int64_t k = lo; k < hi; ++k) m = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m);
+    m *= y[i];  // folded margin b_i a_i . x (exact: b = +-1)
     // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
     acc += fmax(-m, 0.0) + log1p(exp(-fabs(m)));
     if (sig != nullptr) sig[i] = -1.0 / (1.0 + exp(m));
@@ -1584,11 +1596,12 @@ margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restri
   block_partials(acc, x, xs, d, block_out, wl, wq);
 }
 
-// A9 margins over row tiles (see "Row tiles" above): m_i = a~_i . x per row by a
+// A9 margins over row tiles (see "Row tiles" above): m_i = b_i a_i . x per row by a
 // segmented warp reduction, then loss_i = softplus(-m_i), sigma~_i.
 __global__ void __launch_bounds__(256)
 margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-              const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
+              const double* __restrict__ vals, const double* __restrict__ y,
+              const double* __restrict__ x, int xs, int64_t n,
               double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
   __shared__ double rsum[8][32];
   __shared__ double wl[8], wq[8];
@@ -1617,7 +1630,7 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
     }
     __syncwarp();
     if (row) {
-      const double mu = rsum[wib][lane];
+      const double mu = rsum[wib][lane] * y[r0 + lane];  // folded margin
       // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
       acc += fmax(-mu, 0.0) + log1p(exp(-fabs(mu)));
       if (sig != nullptr) sig[r0 + lane] = -1.0 / (1.0 + exp(mu));
@@ -1634,7 +1647,8 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
 template <int G, int U>
 __global__ void __launch_bounds__(256)
 margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
-                   const double* __restrict__ vals, const double* __restrict__ x, int xs, int64_t n,
+                   const double* __restrict__ vals, const double* __restrict__ y,
+                   const double* __restrict__ x, int xs, int64_t n,
                    double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
   constexpr int RG = 32 / G, RPW = RG * U;  // rows per warp batch / per warp iteration
   __shared__ double wl[8], wq[8];
@@ -1667,7 +1681,7 @@ margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t i = r0 + u * RG + q;
-      const double mu = group_sum<G>(m[u], gmask);
+      const double mu = group_sum<G>(m[u], gmask) * (i < n ? y[i] : 1.0);  // folded margin
       if (i < n && g == 0) {
         // softplus(-m) = max(-m, 0) + log1p(exp(-|m|))
         acc += fmax(-mu, 0.0) + log1p(exp(-fabs(mu)));
@@ -1755,13 +1769,14 @@ __global__ void iota_kernel(int64_t* __restrict__ out, int64_t m) {
 
 __global__ void csc_gather_kernel(const int64_t* __restrict__ perm,
                                   const int32_t* __restrict__ row_of,
-                                  const double* __restrict__ vals, int64_t m,
+                                  const double* __restrict__ vals, const double* __restrict__ y, int64_t m,
                                   int32_t* __restrict__ csc_rows, double* __restrict__ csc_vals) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = perm[k];
-    csc_rows[k] = row_of[j];
-    csc_vals[k] = vals[j];
+    const int32_t r = row_of[j];
+    csc_rows[k] = r;
+    csc_vals[k] = vals[j] * y[r];  // folded a~ = b a (exact)
   }
 }
 
