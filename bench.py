@@ -80,37 +80,78 @@ def parse():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
-
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks / clock-event (throttle) reasons sampled every 5 ms during the timed region,
+    in process through NVML (what nvidia-smi reads): no fork of this large CUDA process while
+    the timed steps are being enqueued (spawning nvidia-smi there stalled the enqueueing
+    thread and starved the GPU: c2's ingest phase read 57 instead of 44 us).  Falls back to
+    one background `nvidia-smi -lms 200` started before the timed region."""
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.rows = []
         self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t = None
+        self._proc = None
+        self._nv = None
+        try:
+            import pynvml as nv
 
-    def _run(self):
-        while not self._stop.is_set():
+            nv.nvmlInit()
+            h = None
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                import torch
+
+                pr = torch.cuda.get_device_properties(gpu)
+                bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+                h = nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(gpu)
+            self._nv, self._h = nv, h
+            self._t = threading.Thread(target=self._run_nvml, daemon=True)
+        except Exception:
+            self._nv = None
+
+    def _run_nvml(self):
+        nv, h = self._nv, self._h
+        bits = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(sm), str(mx), ""] + ["Active" if rs & b else "Not Active" for _, b in bits])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            if self._stop.wait(0.005):
+                break
 
     def __enter__(self):
-        self._t.start()
+        if self._t is not None:
+            self._t.start()
+        else:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
+        if self._proc is not None:
+            self._proc.terminate()  # this Popen's own PID
+            try:
+                out = self._proc.communicate(timeout=5)[0]
+            except Exception:
+                out = ""
+            self.rows += [[c.strip() for c in ln.split(",")] for ln in out.splitlines() if ln.strip()]
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def summary(self):
         if not self.rows:
