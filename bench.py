@@ -2,11 +2,11 @@
 
 A "step" = one pass of every SURVEY.md section 8(a) row over one batch of
 synthetic input:
-    A0+A1  asaga_reload_device_async  validate, fold labels, n_v / D / L (non-blocking;
+    A0+A1  asaga_reload_device_async  validate (read-only), n_v / D / L (non-blocking;
                                       the validation is read back by A9's call)
     A2-A8  asaga_run_async(n)      one epoch = n ASAGA updates (c2: the combine kernel,
                                    c3/c4: the plain kernel with the hot split)   1 kernel
-    A9     asaga_objective_device  f at the new iterate                   2 kernels
+    A9     asaga_objective_device  f at the new iterate                   1 kernel
 value = n updates / step time (CUDA events on the context's stream, summed
 over the K timed steps, max over ranks).  512 MiB is written and read back
 between steps, outside the timed events (a cold, clean L2 at every step).  The update kernel runs at the
@@ -430,10 +430,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8, "f_host": f_host},
             # ours per step: ingest_init, ingest (for d <= 4096 its last block also runs the
-            # profile and the report; else profile + report kernels), update, margin, finish,
-            # + expand_d unless every feature is combined, + hot_flag and hot_slot when
-            # combining with d > 4096 (CUB's scan kernels are library, not counted)
-            "gpu_launches": (5 + (0 if p.d <= 4096 else 2)
+            # profile and the report; else profile + report kernels, and A9's dense copy of
+            # x), update, margin (its last block finishes f), + expand_d unless every
+            # feature is combined, + hot_flag and hot_slot when combining with d > 4096
+            # (CUB's scan kernels are library, not counted)
+            "gpu_launches": (4 + (0 if p.d <= 4096 else 3)
                              + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) else 1)
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),

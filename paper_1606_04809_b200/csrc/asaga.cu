@@ -472,7 +472,7 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   }
   TRY(dalloc(ctx, &ctx->block_loss, 2 * (size_t)ctx->obj_blocks));  // loss partials, ||x||^2 partials
   TRY(dalloc(ctx, &ctx->scal, 4));
-  TRY(dalloc(ctx, &ctx->flag, 8));  // [0] non-finite, [1] max n_v, [2] hot count, [3] run guard, [4] ingest blocks
+  TRY(dalloc(ctx, &ctx->flag, 8));  // [0] non-finite, [1] max n_v, [2] hot count, [3] run guard, [4] ingest blocks, [5] objective blocks
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
   if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
@@ -886,23 +886,22 @@ asaga_status ensure_csc(asaga_ctx* ctx) {
 asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, double* f_dev,
                                double* loss_sum_dev, bool want_sig, cudaStream_t s) {
   double* sig = want_sig ? ctx->sig : nullptr;
+  // the margin kernel's last block also finishes f (ticket in flag[5], reset by that block)
+  const ObjFinish fin{ctx->flag + 5, ctx->n, ctx->lambda, f_dev, loss_sum_dev};
   // short rows: G lanes per row (G ~ mean/3); long rows: 32-row tiles streamed flat
   const double mean = (double)ctx->nnz / (double)ctx->n;
   if (mean <= 16.0)
     margin_thread_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
-                                                            ctx->n, sig, ctx->block_loss, ctx->d);
+                                                            ctx->n, sig, ctx->block_loss, ctx->d, fin);
   else if (mean <= 24.0)
     margin_rows_kernel<8, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
-                                                                 ctx->n, sig, ctx->block_loss, ctx->d);
+                                                                 ctx->n, sig, ctx->block_loss, ctx->d, fin);
   else if (ctx->margin_tiles)
     margin_kernel<<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs, ctx->n, sig,
-                                                     ctx->block_loss, ctx->d);
+                                                     ctx->block_loss, ctx->d, fin);
   else
     margin_rows_kernel<32, 4><<<ctx->obj_blocks, kBlock, 0, s>>>(ctx->rowptr, ctx->cols, ctx->vals, ctx->y, x_dev, xs,
-                                                                  ctx->n, sig, ctx->block_loss, ctx->d);
-  CK(ctx, cudaGetLastError());
-  finish_objective_kernel<<<1, 1024, 0, s>>>(ctx->block_loss, ctx->obj_blocks, x_dev, xs, ctx->d,
-                                             ctx->n, ctx->lambda, f_dev, loss_sum_dev);
+                                                                  ctx->n, sig, ctx->block_loss, ctx->d, fin);
   CK(ctx, cudaGetLastError());
   return ASAGA_OK;
 }

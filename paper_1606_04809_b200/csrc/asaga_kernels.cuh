@@ -1551,8 +1551,19 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
 // sigma~_i = -1/(1+exp(m_i)) (so sigma_i a_i = sigma~_i a~_i).
 // A9 block partials in a fixed order: block_out[b] = this block's loss sum and
 // block_out[gridDim.x + b] = its share of ||x||^2 (x strided over the whole grid).
+// A9 finish, fused into the margin kernels: the last block to finish (ticket in ctr, reset
+// by that block) sums the block partials in a fixed order -- f is deterministic.
+struct ObjFinish {
+  int* ctr;
+  int64_t n;
+  double lambda_;
+  double* f_out;     // f = loss / n + lambda/2 ||x||^2 (nullable)
+  double* loss_out;  // sum of the losses (nullable)
+};
+
 __device__ __forceinline__ void block_partials(double acc, const double* __restrict__ x, int xs, int64_t d,
-                                               double* __restrict__ block_out, double* wl, double* wq) {
+                                               double* __restrict__ block_out, double* wl, double* wq,
+                                               const ObjFinish& fin) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double sq = 0.0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d; v += (int64_t)gridDim.x * blockDim.x)
@@ -1564,6 +1575,7 @@ __device__ __forceinline__ void block_partials(double acc, const double* __restr
     wq[wib] = sq;
   }
   __syncthreads();
+  __shared__ int is_last;
   if (threadIdx.x == 0) {
     double s = 0.0, q = 0.0;
     for (int j = 0; j < (int)(blockDim.x >> 5); ++j) {
@@ -1572,6 +1584,33 @@ __device__ __forceinline__ void block_partials(double acc, const double* __restr
     }
     block_out[blockIdx.x] = s;
     block_out[gridDim.x + blockIdx.x] = q;
+    __threadfence();
+    is_last = atomicAdd(fin.ctr, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  __shared__ double s_loss[256], s_sq[256];
+  const int nb = (int)gridDim.x;
+  double a = 0.0, b = 0.0;
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+    a += __ldcg(block_out + j);
+    b += __ldcg(block_out + nb + j);
+  }
+  s_loss[threadIdx.x] = a;
+  s_sq[threadIdx.x] = b;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      s_loss[threadIdx.x] += s_loss[threadIdx.x + off];
+      s_sq[threadIdx.x] += s_sq[threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (fin.f_out) *fin.f_out = s_loss[0] / (double)fin.n + 0.5 * fin.lambda_ * s_sq[0];
+    if (fin.loss_out) *fin.loss_out = s_loss[0];
+    *fin.ctr = 0;  // ready for the next evaluation
   }
 }
 
@@ -1580,7 +1619,7 @@ __global__ void __launch_bounds__(256)
 margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                      const double* __restrict__ vals, const double* __restrict__ y,
                      const double* __restrict__ x, int xs, int64_t n,
-                     double* __restrict__ sig, double* __restrict__ block_out, int64_t d) {
+                     double* __restrict__ sig, double* __restrict__ block_out, int64_t d, ObjFinish fin) {
   __shared__ double wl[8], wq[8];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1593,7 +1632,7 @@ margin_thread_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restri
     acc += fmax(-m, 0.0) + log1p(exp(-fabs(m)));
     if (sig != nullptr) sig[i] = -1.0 / (1.0 + exp(m));
   }
-  block_partials(acc, x, xs, d, block_out, wl, wq);
+  block_partials(acc, x, xs, d, block_out, wl, wq, fin);
 }
 
 // A9 margins over row tiles (see "Row tiles" above): m_i = b_i a_i . x per row by a
@@ -1602,7 +1641,7 @@ __global__ void __launch_bounds__(256)
 margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
               const double* __restrict__ vals, const double* __restrict__ y,
               const double* __restrict__ x, int xs, int64_t n,
-              double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
+              double* __restrict__ sig, double* __restrict__ block_loss, int64_t d, ObjFinish fin) {
   __shared__ double rsum[8][32];
   __shared__ double wl[8], wq[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1637,7 +1676,7 @@ margin_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ co
     }
     __syncwarp();
   }
-  block_partials(acc, x, xs, d, block_loss, wl, wq);
+  block_partials(acc, x, xs, d, block_loss, wl, wq, fin);
 }
 
 // A9 margins for short rows (mean <= 32): G lanes per row, a warp streams U batches of
@@ -1649,7 +1688,7 @@ __global__ void __launch_bounds__(256)
 margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ cols,
                    const double* __restrict__ vals, const double* __restrict__ y,
                    const double* __restrict__ x, int xs, int64_t n,
-                   double* __restrict__ sig, double* __restrict__ block_loss, int64_t d) {
+                   double* __restrict__ sig, double* __restrict__ block_loss, int64_t d, ObjFinish fin) {
   constexpr int RG = 32 / G, RPW = RG * U;  // rows per warp batch / per warp iteration
   __shared__ double wl[8], wq[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1689,35 +1728,7 @@ margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict
       }
     }
   }
-  block_partials(acc, x, xs, d, block_loss, wl, wq);
-}
-
-// Single block: f = (sum of loss partials) / n + lambda/2 (sum of ||x||^2 partials); also the
-// raw loss sum.  (x, xs, d unused: the partials come from the margin kernel.)
-__global__ void __launch_bounds__(1024)
-finish_objective_kernel(const double* __restrict__ block_loss, int nblocks,
-                        const double* __restrict__ x, int xs, int64_t d, int64_t n, double lambda_,
-                        double* __restrict__ f_out, double* __restrict__ loss_sum_out) {
-  __shared__ double s_loss[1024], s_sq[1024];
-  double a = 0.0, b = 0.0;  // the margin kernel's block partials: loss sums, then ||x||^2 shares
-  for (int j = threadIdx.x; j < nblocks; j += blockDim.x) {
-    a += block_loss[j];
-    b += block_loss[nblocks + j];
-  }
-  s_loss[threadIdx.x] = a;
-  s_sq[threadIdx.x] = b;
-  __syncthreads();
-  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-    if ((int)threadIdx.x < off) {
-      s_loss[threadIdx.x] += s_loss[threadIdx.x + off];
-      s_sq[threadIdx.x] += s_sq[threadIdx.x + off];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    if (f_out) *f_out = s_loss[0] / (double)n + 0.5 * lambda_ * s_sq[0];
-    if (loss_sum_out) *loss_sum_out = s_loss[0];
-  }
+  block_partials(acc, x, xs, d, block_loss, wl, wq, fin);
 }
 
 // CSC segments: segment s covers csc entries [seg_lo[s], seg_hi[s]) of one column.
