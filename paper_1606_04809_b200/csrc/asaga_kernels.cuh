@@ -103,6 +103,23 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
                "l"(gmem) : "memory");
 }
+// Streaming copies (row data read once per sample) marked L2 evict-first, so they do not
+// push the shared state ({x, abar} pairs: 52 MB on c4) out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async4_ef(void* smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void cp_async8_ef(void* smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 template <int N>
@@ -745,14 +762,15 @@ __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, c
   double* sd = sv + P;
   int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
   const int len = (int)(hi - lo);
+  const uint64_t pol = policy_evict_first();
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     if (j * G >= len) break;  // group-uniform: no predicated-off chunks
     const int64_t k = lo + j * G + g;
     if (j * G + g < len) {
-      cp_async4(sc + j * G + g, cols + k);
-      cp_async8(sv + j * G + g, vals + k);
-      cp_async8(sd + j * G + g, dv + k);
+      cp_async4_ef(sc + j * G + g, cols + k, pol);
+      cp_async8_ef(sv + j * G + g, vals + k, pol);
+      cp_async8_ef(sd + j * G + g, dv + k, pol);
     }
   }
   cp_async_commit();
