@@ -212,6 +212,15 @@ ASAGA_API asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view*
 ASAGA_API asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A_dev,
                                                  const double* y_dev);
 
+/* As asaga_reload, but NON-blocking: the HOST arrays are copied on the context's own copy
+ * stream into one of two device buffers used in turn, so the copy of the next matrix runs
+ * while the compute stream still works on the previous one (page-locked host memory is
+ * needed for the copy to be asynchronous; pageable memory works but the copy then blocks
+ * the caller).  The caller keeps the host arrays unchanged until the next blocking call.
+ * Validation, the run guard and ASAGA_E_STATE are as in asaga_reload_device_async; without
+ * a previous successful ingest it behaves as asaga_reload. */
+ASAGA_API asaga_status asaga_reload_async(asaga_ctx* ctx, const asaga_csr_view* A, const double* y);
+
 /* Process the global update counters t = t0 .. t0+n_updates-1 (t0 = the
  * context's counter, then t0 += n_updates).  Update t uses row
  * i_t = floor(r_t * n / 2^64), r_t = the first two 32-bit words of

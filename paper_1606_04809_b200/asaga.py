@@ -79,6 +79,8 @@ ABI_FUNCTIONS = {
                                            ctypes.c_void_p]),
     "asaga_reload_device_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsrView),
                                                  ctypes.c_void_p]),
+    "asaga_reload_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsrView),
+                                                 ctypes.c_void_p]),
     "asaga_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]),
     "asaga_run_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]),
     "asaga_objective": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _F64P]),
@@ -247,13 +249,23 @@ class Asaga:
         self._keep = (indptr, indices, data, y) if dev else None  # borrowed device arrays
 
     def reload_async(self, indptr, indices, data, y) -> None:
-        """Non-blocking device re-ingest (CUDA tensors, borrowed by the context until the
-        next reload / close); validation is reported by the next blocking call."""
-        assert _is_cuda(indptr), "reload_async takes device (CUDA) arrays"
+        """Non-blocking re-ingest; validation is reported by the next blocking call.
+        CUDA tensors: borrowed by the context until the next reload / close
+        (asaga_reload_device_async).  Host arrays (page-locked for the copy to overlap
+        earlier work): copied on the context's copy stream into one of two device buffers
+        (asaga_reload_async); they must stay unchanged until the next blocking call."""
+        dev = _is_cuda(indptr)
+        if not dev:
+            indptr, indices = _host(indptr, np.int64), _host(indices, np.int32)
+            data, y = _host(data, np.float64), _host(y, np.float64)
         view = CsrView(int(indptr.shape[0]) - 1, self.d, int(indices.shape[0]), _ptr(indptr),
                        _ptr(indices), _ptr(data))
-        self._keep = (indptr, indices, data, y)
-        _check(_lib.asaga_reload_device_async(self._h, ctypes.byref(view), _ptr(y)), self._h)
+        if dev:
+            self._keep = (indptr, indices, data, y)
+        else:
+            self._keep_host = (indptr, indices, data, y)
+        fn = _lib.asaga_reload_device_async if dev else _lib.asaga_reload_async
+        _check(fn(self._h, ctypes.byref(view), _ptr(y)), self._h)
 
     def run(self, n_updates: int, seed: int) -> None:
         _check(_lib.asaga_run(self._h, int(n_updates), int(seed)), self._h)

@@ -58,6 +58,19 @@ struct asaga_ctx {
   int32_t* own_cols = nullptr;
   double* own_vals = nullptr;
   double* own_y = nullptr;
+  // asaga_reload_async (host arrays): two device copies used in turn, filled on copy_stream
+  // while the compute stream still works on the other one
+  struct HostSet {
+    int64_t* rowptr = nullptr;
+    int32_t* cols = nullptr;
+    double* vals = nullptr;
+    double* y = nullptr;
+    cudaEvent_t copied = nullptr;  // H2D into this set done (copy stream)
+    cudaEvent_t free = nullptr;    // the compute stream's last use of this set done
+    bool used = false;
+  } hs[2];
+  int hs_next = 0;
+  cudaStream_t copy_stream = nullptr;
   double2* xa = nullptr;   // {x_v, abar_v} pairs at xa[v * S]
   int S = 1;               // pair stride
   double bulk_dmax = 0.0;  // hybrid scatter threshold on D_c (MODE 2)
@@ -1118,6 +1131,46 @@ asaga_status asaga_reload_device_async(asaga_ctx* ctx, const asaga_csr_view* A, 
   return ASAGA_OK;
 }
 
+asaga_status asaga_reload_async(asaga_ctx* ctx, const asaga_csr_view* A, const double* y) {
+  TRY(check_same_shape(ctx, A, y));
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // (also: the previous asynchronous copy has landed)
+  if (!ctx->shape_valid) return asaga_reload(ctx, A, y);  // no launch shape to keep yet
+  if (!ctx->copy_stream) CK(ctx, cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  const int b = ctx->hs_next;
+  asaga_ctx::HostSet& h = ctx->hs[b];
+  if (!h.rowptr) {
+    TRY(dalloc(ctx, &h.rowptr, ctx->n + 1));
+    TRY(dalloc(ctx, &h.cols, ctx->nnz));
+    TRY(dalloc(ctx, &h.vals, ctx->nnz));
+    TRY(dalloc(ctx, &h.y, ctx->n));
+    CK(ctx, cudaEventCreateWithFlags(&h.copied, cudaEventDisableTiming));
+    CK(ctx, cudaEventCreateWithFlags(&h.free, cudaEventDisableTiming));
+  }
+  // the copy may start once the compute stream is done with this set's previous contents
+  if (h.used) CK(ctx, cudaStreamWaitEvent(ctx->copy_stream, h.free, 0));
+  CK(ctx, cudaMemcpyAsync(h.rowptr, A->indptr, sizeof(int64_t) * (ctx->n + 1), cudaMemcpyHostToDevice,
+                          ctx->copy_stream));
+  CK(ctx, cudaMemcpyAsync(h.cols, A->indices, sizeof(int32_t) * ctx->nnz, cudaMemcpyHostToDevice,
+                          ctx->copy_stream));
+  CK(ctx, cudaMemcpyAsync(h.vals, A->data, sizeof(double) * ctx->nnz, cudaMemcpyHostToDevice,
+                          ctx->copy_stream));
+  CK(ctx, cudaMemcpyAsync(h.y, y, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->copy_stream));
+  CK(ctx, cudaEventRecord(h.copied, ctx->copy_stream));
+  // compute stream: everything enqueued so far read the other set (or the caller's arrays)
+  asaga_ctx::HostSet& o = ctx->hs[1 - b];
+  if (o.used) CK(ctx, cudaEventRecord(o.free, ctx->stream));
+  CK(ctx, cudaStreamWaitEvent(ctx->stream, h.copied, 0));
+  h.used = true;
+  ctx->hs_next = 1 - b;
+  TRY(ingest_enqueue(ctx, h.rowptr, h.cols, h.vals, h.y, true));
+  TRY(enqueue_expand(ctx));
+  TRY(enqueue_report(ctx, true));
+  ctx->t = 0;
+  ctx->ing_pending = true;
+  return ASAGA_OK;
+}
+
 asaga_status asaga_run_async(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed) {
   if (!ctx) return fail(nullptr, ASAGA_E_INVALID_ARG, "ctx is NULL");
   CK(ctx, cudaSetDevice(ctx->device));
@@ -1437,6 +1490,14 @@ void asaga_destroy(asaga_ctx* ctx) {
   if (ctx->ev_ing) cudaEventDestroy(ctx->ev_ing);
   if (ctx->h_ing) cudaFreeHost(ctx->h_ing);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  for (auto& h : ctx->hs) {
+    if (h.copied) cudaEventDestroy(h.copied);
+    if (h.free) cudaEventDestroy(h.free);
+  }
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

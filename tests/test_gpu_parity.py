@@ -176,6 +176,77 @@ def test_device_inputs_match_host_inputs():
         assert np.array_equal(u, v)
 
 
+@gpu
+def test_borrowed_device_arrays_and_host_reloads_interleave():
+    """Device inputs are borrowed (the context reads the caller's arrays, asaga.h), host
+    inputs go to the context's own copy; reloads switch between the two.  Each matrix gives
+    the oracle's f and gradient, and a same-shape second matrix with flipped labels is
+    picked up by every kernel that applies b_i (objective, gradient, deterministic run)."""
+    import torch
+
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=3000)
+    q = datagen.Problem("flip", p.n, p.d, p.indptr, p.indices, p.data, -p.y, p.lam)
+    g = gamma_of(p)
+    t = lambda arr: torch.from_numpy(arr).cuda()
+    x = np.random.default_rng(3).standard_normal(p.d) * 0.3
+    a = m.Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, g, deterministic=True)
+    for src, prob in (("dev", p), ("host", q), ("dev", q), ("host", p), ("dev", p)):
+        if src == "dev":
+            a.reload(t(prob.indptr), t(prob.indices), t(prob.data), t(prob.y))
+        else:
+            a.reload(prob.indptr, prob.indices, prob.data, prob.y)
+        assert a.objective(x) == pytest.approx(oracle.objective(prob, prob.y, prob.lam, x), rel=1e-12)
+        assert rel(a.full_grad(x), oracle.full_grad(prob, prob.y, prob.lam, x)) <= 1e-10
+        a.run(2 * prob.n, SEED)
+        r = oracle.sparse_saga(prob, prob.y, prob.lam, g, SEED, 2 * prob.n)
+        xg, alg, abg, _ = a.get_state()
+        assert rel(xg, r.x) <= 1e-9 and rel(alg, r.alpha) <= 1e-9 and rel(abg, r.alpha_bar) <= 1e-9
+    a.close()
+
+
+@gpu
+def test_host_reload_async_double_buffered():
+    """asaga_reload_async: host matrices copied on the copy stream into two device buffers
+    used in turn.  Alternating matrices (labels flipped) enqueued back to back, each followed
+    by a deterministic run: every run matches the oracle on ITS matrix (no buffer is
+    overwritten while read), and a bad label surfaces at the next blocking call."""
+    import torch
+
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=3000)
+    q = datagen.Problem("flip", p.n, p.d, p.indptr, p.indices, p.data, -p.y, p.lam)
+    g = gamma_of(p)
+    pin = lambda arr: torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    probs = [q, p, q, q, p]
+    host = [tuple(pin(v) for v in (pr.indptr, pr.indices, pr.data, pr.y)) for pr in probs]
+    f_dev = torch.zeros(len(probs), dtype=torch.float64, device="cuda")
+    x_after = []
+    for k, pr in enumerate(probs):
+        a.reload_async(*host[k])
+        a.run_async(pr.n, SEED)
+        a.objective_device(f_dev[k:k + 1])
+        if k % 2 == 1:  # a blocking call now and then (resolves the pending validation)
+            x_after.append((k, a.get_state()[0]))
+    torch.cuda.synchronize()
+    a.stats()
+    fs = f_dev.cpu().numpy()
+    for k, pr in enumerate(probs):
+        r = oracle.sparse_saga(pr, pr.y, pr.lam, g, SEED, pr.n)
+        assert fs[k] == pytest.approx(oracle.objective(pr, pr.y, pr.lam, r.x), rel=1e-9), k
+    for k, xg in x_after:
+        r = oracle.sparse_saga(probs[k], probs[k].y, p.lam, g, SEED, p.n)
+        assert rel(xg, r.x) <= 1e-9
+    bad_y = p.y.copy()
+    bad_y[17] = 0.0
+    a.reload_async(pin(p.indptr), pin(p.indices), pin(p.data), pin(bad_y))
+    with pytest.raises(m.AsagaError) as ei:
+        a.objective()
+    assert ei.value.name == "ASAGA_E_BAD_LABEL" and "row 17" in str(ei.value)
+    a.close()
+
+
 # ---------------------------------------------------------------------- A9 objective / gradient
 @gpu
 def test_objective_and_gradient(prob):
