@@ -216,13 +216,13 @@ __device__ __forceinline__ void report_body(const unsigned long long* __restrict
                                             int* __restrict__ flag, unsigned long long* host_out,
                                             int64_t row_cap, int hot_expected, int guard);
 
-// A0 + A1 over row tiles: validate, copy rowptr / cols / y, fold labels into the
-// values, count n_v (shared histogram when d fits), max ||a_i||^2, longest row.
+// A0 + A1 over row tiles, reading the matrix only: validate, count n_v (shared histogram
+// when d fits), max ||a_i||^2, longest row.
 // STAGED (short rows): a tile whose entries fit kStageCap is copied into the warp's
-// shared stage with coalesced loads, each row is then checked / folded / counted by its
-// OWNER lane from shared memory (the previous index and ||a_i||^2 in registers: a few
-// instructions per entry instead of the flat path's per-chunk row search and segmented
-// reduction), and the tile is written back coalesced.  Larger tiles take the flat path.
+// shared stage by cp.async, each row is then checked / counted by its OWNER lane from
+// shared memory (the previous index and ||a_i||^2 in registers: a few instructions per
+// entry instead of the flat path's per-chunk row search and segmented reduction).
+// Larger tiles take the flat path.
 // ROWS (long rows, mean >= 32 entries, n_v through the hash cache): the warp walks the
 // tile row by row, 32 entries of one row per chunk: the row, label and previous column
 // are warp-uniform, so the flat path's per-chunk row search and segmented reduction (186
@@ -1418,7 +1418,7 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
       const int32_t* sc = reinterpret_cast<const int32_t*>(sv + (FULL ? P : 2 * P));
       const int32_t* ss = sc + P;
       const double ai = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off);
-      const double bi = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off + 8);
+      const double yb = *reinterpret_cast<const double*>(gbase + stage * SM::stage_bytes + SM::alpha_off + 8);
       double2 xb[NR];
       double qq[NR];
 #pragma unroll
@@ -1449,10 +1449,10 @@ __global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
         dot = fma(ld_nc_f64(p.vals + k), v.x, dot);
         qs[kk - P] = s >= 0 ? v.y : ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
       }
-      dot = group_sum<G>(dot, gmask) * bi;  // folded margin (exact: b = +-1)
+      dot = group_sum<G>(dot, gmask) * yb;  // folded margin (exact: b = +-1)
       // sigma~ = -1/(1+exp(m)); the correctly rounded reciprocal equals the IEEE division
       const double da = -__drcp_rn(1.0 + exp(dot)) - ai;
-      const double db = da * bi;  // dalpha a~_k = (dalpha b_i) a_k, exact
+      const double db = da * yb;  // dalpha a~_k = (dalpha b_i) a_k, exact
       const double ngam = -p.gamma;
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
