@@ -53,7 +53,8 @@ OPERATING_POINT = {
 def asaga_options(op):
     """Asaga keyword options of an operating point."""
     return dict(bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
-                smem_replica_refresh=op["repl"], combine_min_freq=op["comb"])
+                smem_replica_refresh=op["repl"], combine_min_freq=op["comb"],
+                l2_persist_state=bool(op.get("persist", False)))
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -72,6 +73,7 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--concurrency", type=int, default=None, help="samples in flight")
     ap.add_argument("--gamma-scale", type=float, default=None)
+    ap.add_argument("--l2-persist", type=int, default=None, help="override l2_persist_state (0/1)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-6 run")
@@ -278,7 +280,9 @@ def main():
     from paper_1606_04809_b200 import Asaga
 
     p = datagen.make(args.workload)
-    op = OPERATING_POINT[args.workload]
+    op = dict(OPERATING_POINT[args.workload])
+    if args.l2_persist is not None:
+        op["persist"] = bool(args.l2_persist)
     W = args.concurrency if args.concurrency is not None else op["W"]
     gscale = args.gamma_scale if args.gamma_scale is not None else op["gscale"]
     bulk = op["bulk"]

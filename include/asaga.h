@@ -140,6 +140,10 @@ typedef struct {
                             samples in flight are packed into fewer, fuller blocks so each
                             communication pass carries more combined adds.  0 (default) = one
                             block per SM (per resident cluster slot). */
+  int l2_persist_state;  /* 1: the plain update kernel is launched with an L2 access-policy
+                            window marking the {x, abar} pair array persisting (up to the
+                            device's persisting carve-out, which this raises for the process;
+                            SURVEY 8(d) M6).  0 (default) = off. */
 } asaga_options;
 
 typedef struct {

@@ -85,6 +85,7 @@ struct asaga_ctx {
   int comb_csize = 1;          // blocks per cluster of the combine kernel
   int comb_cluster_opt = 0;    // requested cluster size (0 = 1)
   int comb_max_blocks = 0;     // cap on the combine kernel's blocks (0 = resident capacity)
+  int l2_persist = 0;          // plain kernel: L2 access-policy window (persisting) over xa
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
@@ -787,6 +788,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
     return fail(ctx, ASAGA_E_INVALID_ARG, "combine_max_blocks must be >= 0 (got %d)", o.combine_max_blocks);
   }
   ctx->comb_max_blocks = o.combine_max_blocks;
+  ctx->l2_persist = o.l2_persist_state ? 1 : 0;
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
@@ -1023,8 +1025,36 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   const size_t smem = replica_bytes(ctx) + (size_t)(block / ctx->lanes) * ctx->group_bytes;
   CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
-  void* args[] = {&p};
-  CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(block), args, smem, ctx->stream));
+  if (ctx->l2_persist) {
+    // the {x, abar} pairs as a persisting L2 window for this launch only
+    // (the device's persisting carve-out is set once per context, at most its maximum)
+    int max_win = 0, max_persist = 0;
+    CK(ctx, cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+    CK(ctx, cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+    const size_t bytes = std::min<size_t>((size_t)ctx->d * ctx->S * sizeof(double2), (size_t)max_win);
+    size_t cur = 0;
+    CK(ctx, cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    const size_t want = std::min<size_t>(bytes, (size_t)max_persist);
+    if (cur < want) CK(ctx, cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[0].val.accessPolicyWindow.base_ptr = ctx->xa;
+    attr[0].val.accessPolicyWindow.num_bytes = bytes;
+    attr[0].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)want / (double)bytes);
+    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(ctx, cudaLaunchKernelEx(&cfg, fn, p));
+  } else {
+    void* args[] = {&p};
+    CK(ctx, cudaLaunchKernel((const void*)fn, dim3(grid), dim3(block), args, smem, ctx->stream));
+  }
   if (timed) CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
   ctx->t += n_updates;
   return ASAGA_OK;
@@ -1052,6 +1082,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->combine_cluster = 0;
   opt->combine_write_through = 0;
   opt->combine_max_blocks = 0;
+  opt->l2_persist_state = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--lanes", type=int, default=0, help="lanes_per_sample")
     ap.add_argument("--wt", action="store_true", help="combine_write_through")
     ap.add_argument("--maxblocks", type=int, default=0, help="combine_max_blocks")
+    ap.add_argument("--persist", action="store_true", help="l2_persist_state")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -52,7 +53,8 @@ def main():
               hot_split_min_freq=args.split,
               smem_replica_refresh=args.repl, combine_min_freq=args.comb,
               combine_cluster=args.cluster, lanes_per_sample=args.lanes,
-              combine_write_through=args.wt, combine_max_blocks=args.maxblocks)
+              combine_write_through=args.wt, combine_max_blocks=args.maxblocks,
+              l2_persist_state=args.persist)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     for W in [int(c) for c in args.conc.split(",")]:
