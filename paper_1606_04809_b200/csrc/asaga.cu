@@ -247,7 +247,6 @@ UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
 
 constexpr int64_t kReplicaMaxD = 4096;  // 64 KiB of {x, abar} pairs per block
 constexpr int kCombMaxH = 4096;         // hot features combined per block: 128 KiB of xr + pend
-constexpr int kCombBlock = 512;         // max threads of a combine block (launch bounds)
 
 bool use_combine(const asaga_ctx* ctx) {
   // comb_H == 0 (no feature that popular): the same pipelined kernel, no communication warp
@@ -296,6 +295,7 @@ size_t comb_smem(const asaga_ctx* ctx, int nwb) {  // xr, pend, D table, worker 
 // resident at once (every block runs for the whole launch).  nwb = worker groups per block.
 asaga_status comb_shape(asaga_ctx* ctx, int64_t workers, int* nwb, int* blocks, int* csize,
                         int64_t* workers_out) {
+  const int kCombBlock = comb_block_threads(ctx->nr);  // launch bounds of the instance
   const int per_warp = 32 / ctx->lanes;
   int C = ctx->comb_cluster_opt > 0 ? ctx->comb_cluster_opt : 1;
   C = std::max(1, std::min(C, 8));

@@ -1207,8 +1207,13 @@ __device__ __forceinline__ void issue_row_copy_c(unsigned char* base, int stage,
   cp_async_commit();
 }
 
+// Block size (launch bounds): 768 threads -- up to 46 workers of 16 lanes + the
+// communication warp per SM at <= 80 registers, no spills (512-thread blocks capped c2 at
+// W = 4440, 1024 forced 64 registers; profiles/r01_combine_kernel.md); 512 for NR = 8 (long
+// rows), whose register queues would spill at 80.
+__host__ __device__ constexpr int comb_block_threads(int nr) { return nr >= 8 ? 512 : 768; }
 template <int G, int NR, bool FULL>
-__global__ void __launch_bounds__(512, 1) asaga_combine_kernel(UpdateParams p) {
+__global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kernel(UpdateParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (p.ok != nullptr && *reinterpret_cast<const volatile int*>(p.ok) == 0) return;  // run guard (whole grid)
   constexpr int P = NR * G;
