@@ -302,6 +302,13 @@ ASAGA_API asaga_status asaga_stats(const asaga_ctx* ctx, asaga_stats_t* out);
 ASAGA_API asaga_status asaga_sample_indices(int device, uint64_t seed, uint64_t t0, uint64_t count,
                                   uint64_t n, int64_t* out_dev, void* stream);
 
+/* The scalar derivative alone (A5; Alg. 2 lines 6-8, folded logistic
+ * PAPER.md:483-485): out_dev[k] = -1 / (1 + exp(m_dev[k])) as the update kernels compute it
+ * (fp64, a few ulp), for n DEVICE doubles, enqueued on `stream` (NULL = default stream of
+ * `device`).  A test hook: the kernels use the same device function. */
+ASAGA_API asaga_status asaga_debug_sigma(int device, const double* m_dev, double* out_dev, int64_t n,
+                                         void* stream);
+
 /* Device pointer of the context's stream (cudaStream_t). */
 ASAGA_API void* asaga_stream(const asaga_ctx* ctx);
 

@@ -5,6 +5,6 @@ its thin Python binding plus the multi-GPU plumbing (``sharded``) that uses
 ``torch.distributed`` over NCCL.  Importing it loads the CUDA library and fails
 loudly if it is missing -- there is no CPU fallback.
 """
-from .asaga import Asaga, AsagaError, sample_indices  # noqa: F401
+from .asaga import Asaga, AsagaError, debug_sigma, sample_indices  # noqa: F401
 
-__all__ = ["Asaga", "AsagaError", "sample_indices"]
+__all__ = ["Asaga", "AsagaError", "debug_sigma", "sample_indices"]

@@ -99,6 +99,8 @@ ABI_FUNCTIONS = {
     "asaga_snapshot": (ctypes.c_int, [ctypes.c_void_p]),
     "asaga_set_concurrency": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     "asaga_stats": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(Stats)]),
+    "asaga_debug_sigma": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                         ctypes.c_void_p]),
     "asaga_sample_indices": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
                                             ctypes.c_void_p]),
@@ -351,3 +353,10 @@ def sample_indices(seed: int, t0: int, count: int, n: int, out_dev, device: int 
     """Fill the int64 CUDA tensor ``out_dev`` with i_{t0..t0+count-1} (the kernel's sampler)."""
     _check(_lib.asaga_sample_indices(device, int(seed), int(t0), int(count), int(n),
                                      _ptr(out_dev), stream))
+
+
+def debug_sigma(m_dev, out_dev, device: int = 0, stream=None) -> None:
+    """out_dev = -1 / (1 + exp(m_dev)) by the update kernels' device function (CUDA float64
+    tensors of equal length; a test hook)."""
+    assert m_dev.numel() == out_dev.numel()
+    _check(_lib.asaga_debug_sigma(device, _ptr(m_dev), _ptr(out_dev), int(m_dev.numel()), stream))

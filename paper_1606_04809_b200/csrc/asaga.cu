@@ -1434,6 +1434,18 @@ asaga_status asaga_sample_indices(int device, uint64_t seed, uint64_t t0, uint64
   return ASAGA_OK;
 }
 
+asaga_status asaga_debug_sigma(int device, const double* m_dev, double* out_dev, int64_t n, void* stream) {
+  if ((!m_dev || !out_dev) && n > 0) return fail(nullptr, ASAGA_E_INVALID_ARG, "NULL buffer");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, ASAGA_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  if (n <= 0) return ASAGA_OK;
+  int grid = (int)std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 16);
+  sigma_kernel<<<grid, kBlock, 0, (cudaStream_t)stream>>>(m_dev, out_dev, n);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(nullptr, ASAGA_E_CUDA, "sigma_kernel: %s", cudaGetErrorString(e));
+  return ASAGA_OK;
+}
+
 void* asaga_stream(const asaga_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 const char* asaga_last_error(const asaga_ctx* ctx) {

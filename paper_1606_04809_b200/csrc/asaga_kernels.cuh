@@ -127,6 +127,47 @@ __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.w
 __device__ __forceinline__ int ld_nc_i32(const int32_t* p) { return __ldg(p); }
 __device__ __forceinline__ double ld_nc_f64(const double* p) { return __ldg(p); }
 
+// A5 (Alg. 2 lines 6-8; folded logistic P:483-485): sigma~(m) = -1 / (1 + exp(m)) in
+// fp64, ~28 instructions: t = exp(-|m|) by Cody-Waite reduction (k = rint(-|m| / ln 2),
+// r = -|m| - k ln 2 with ln 2 in two parts, |r| <= ln2/2), the degree-12 Taylor polynomial
+// (truncation < 1.6e-16 relative; coefficients 1/j! from constant memory, so the DFMAs take
+// them as operands instead of materialising 64-bit immediates), 2^k added to the exponent
+// field; then 1/(1+t) (1+t in (1, 2]) from the MUFU reciprocal seed and two Newton steps;
+// sigma~ = -t/(1+t) for m >= 0, -1/(1+t) for m < 0.  |m| is clamped at 700 (exp(-700) ~ 1e-304:
+// t stays normal; the lost tail is below 1e-304 absolute).  The library exp + __drcp_rn took
+// 61 warp instructions per sample pair in the combine kernel (ncu, profiles/r01_combine_kernel.md).
+__constant__ double c_inv_fact[13] = {
+    1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0,
+    1.0 / 5040.0,      1.0 / 720.0,      1.0 / 120.0,     1.0 / 24.0,     1.0 / 6.0,
+    0.5,               1.0,              1.0};
+__device__ __forceinline__ double sigma_folded(double m) {
+  const double x = fmax(-fabs(m), -700.0);
+  const double kd = fma(x, 1.4426950408889634, 6755399441055744.0);  // 1.5 * 2^52: rint in the low word
+  const double kf = kd - 6755399441055744.0;
+  double r = fma(kf, -6.93147180559945286227e-01, x);  // ln 2, high part
+  r = fma(kf, -2.31904681384629955842e-17, r);          // ln 2, low part
+  double p = c_inv_fact[0];
+#pragma unroll
+  for (int j = 1; j < 13; ++j) p = fma(p, r, c_inv_fact[j]);
+  const int ki = __double2loint(kd);
+  const double t = __hiloint2double(__double2hiint(p) + (ki << 20), __double2loint(p));
+  const double dd = 1.0 + t;
+  double rc;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(dd));
+  double e = fma(-dd, rc, 1.0);
+  e = fma(e, e, e);
+  rc = fma(rc, e, rc);
+  e = fma(-dd, rc, 1.0);
+  rc = fma(rc, e, rc);
+  return m >= 0.0 ? -t * rc : -rc;
+}
+
+// Test hook (asaga_debug_sigma): sigma_folded over a device array.
+__global__ void sigma_kernel(const double* __restrict__ m, double* __restrict__ out, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = sigma_folded(m[k]);
+}
+
 template <int G>
 __device__ __forceinline__ double group_sum(double v, unsigned mask) {
 #pragma unroll
@@ -948,9 +989,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     // ---- scalar derivative (folded logistic) and memory difference
     dot = group_sum<G>(dot, gmask) * yb;  // folded margin b_i a_i . x^ (exact: b = +-1)
 #ifdef ASAGA_TIMING
-    const double sig = (p.debug_mode & 2) ? -0.5 + 0.0 * dot : -1.0 / (1.0 + exp(dot));
+    const double sig = (p.debug_mode & 2) ? -0.5 + 0.0 * dot : sigma_folded(dot);
 #else
-    const double sig = -__drcp_rn(1.0 + exp(dot));  // correctly rounded: == -1.0 / (1 + e)
+    const double sig = sigma_folded(dot);
 #endif
     const double da = sig - ai;
     const double db = da * yb;  // dalpha a~_k = (dalpha b_i) a_k, exact
@@ -1455,8 +1496,7 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
         qs[kk - P] = s >= 0 ? v.y : ld_nc_f64(p.dv + k) * fma(p.lambda_, v.x, v.y);
       }
       dot = group_sum<G>(dot, gmask) * yb;  // folded margin (exact: b = +-1)
-      // sigma~ = -1/(1+exp(m)); the correctly rounded reciprocal equals the IEEE division
-      const double da = -__drcp_rn(1.0 + exp(dot)) - ai;
+      const double da = sigma_folded(dot) - ai;  // sigma~ = -1/(1+exp(m))
       const double db = da * yb;  // dalpha a~_k = (dalpha b_i) a_k, exact
       const double ngam = -p.gamma;
 #pragma unroll

@@ -74,6 +74,39 @@ def test_sampler_bitexact(n, seed, t0):
     assert np.array_equal(out.cpu().numpy(), oracle.sample_stream(seed, t0, count, n))
 
 
+# ---------------------------------------------------------------------- A5 scalar derivative
+@gpu
+def test_sigma_device_function_accuracy():
+    """A5's sigma~(m) = -1/(1+exp(m)) as the update kernels compute it,
+    against an extended-precision reference (numpy longdouble: 64-bit mantissa) on 2e6
+    margins over [-750, 750], dense near 0, plus special points: within 4 ulp of the
+    reference for |m| <= 700 (and within 1e-300 absolute beyond, where the tail is clamped),
+    exactly -1/2 at 0, increasing in m (up to rounding) and in [-1, 0]."""
+    import torch
+
+    m = asaga_mod()
+    rng = np.random.default_rng(160)
+    z = np.concatenate([rng.uniform(-750, 750, 10**6), rng.standard_normal(10**6) * 3,
+                        [0.0, -0.0, 1e-300, -1e-300, 1e-8, -1e-8, 36.0, -36.0, 700.0, -700.0,
+                         708.0, -708.0, 745.0, -745.0, 1e4, -1e4]])
+    zd = torch.from_numpy(z).cuda()
+    out = torch.empty_like(zd)
+    m.debug_sigma(zd, out)
+    got = out.cpu().numpy()
+    zl = z.astype(np.longdouble)
+    ref = -1.0 / (1.0 + np.exp(zl))
+    inside = np.abs(z) <= 700
+    ulp = np.spacing(np.abs(ref[inside]).astype(np.float64))
+    err = np.abs(got[inside].astype(np.longdouble) - ref[inside]) / ulp
+    assert float(err.max()) <= 4.0, float(err.max())
+    assert np.all(np.abs(got[~inside] - ref[~inside].astype(np.float64)) <= 1e-300)
+    assert got[np.argmax(z == 0.0)] == -0.5
+    assert np.all(got <= 0.0) and np.all(got >= -1.0)
+    order = np.argsort(z, kind="stable")  # monotone up to rounding (a few ulp)
+    g = got[order]
+    assert np.all(np.diff(g) >= -4 * np.spacing(np.abs(g[1:])))
+
+
 # ---------------------------------------------------------------------- A2..A8 deterministic
 def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0):
     m = asaga_mod()
