@@ -909,7 +909,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   int ov_local = 0, ov_iter = 0;
   while (true) {
     // overlap estimate (App. D): progress counter at the read and after the write
-    const bool ov_meas = p.ov != nullptr && (ov_iter++ % p.ov_every) == 0;
+    bool ov_meas = false;
+    if (p.ov != nullptr) ov_meas = (ov_iter++ % p.ov_every) == 0;
     unsigned long long ov_c0 = 0;
     if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
     // ---- pass 1: row entries (shared memory), gathers, dot product
@@ -974,7 +975,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
       }
     }
-    for (int64_t k = lo + P + g; k < hi; k += G) {  // long rows only
+    if (len > P)  // group-uniform: long rows only
+    for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
       const double Dv = ld_nc_f64(p.dv + k);
@@ -1038,6 +1040,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       }
       bulk_commit();
     }
+    if (len > P)  // group-uniform: long rows only
     for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
@@ -1451,7 +1454,8 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
     // this worker's samples: t_first + mW < tend  (32-bit counts from here on)
     const int nsamp = (int)((tend - t_first + W - 1) / W);
     for (int m = 0;; ++m) {
-      const bool ov_meas = p.ov != nullptr && (ov_iter++ % p.ov_every) == 0;
+      bool ov_meas = false;
+    if (p.ov != nullptr) ov_meas = (ov_iter++ % p.ov_every) == 0;
       unsigned long long ov_c0 = 0;
       if (ov_meas) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(ov_c0) : "l"(p.ov));
       cp_async_wait_group<KS - 1>();  // this sample's stage (and bounds of m + KS) landed
@@ -1487,7 +1491,8 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
                                                         : sd[j * G + g] * fma(p.lambda_, xb[j].x, xb[j].y);
         }
       }
-      for (int kk = P + g; kk < len; kk += G) {  // long rows only
+      if (len > P)  // group-uniform: long rows only
+      for (int kk = P + g; kk < len; kk += G) {
         const int64_t k = lo + kk;
         const int c = ld_nc_i32(p.cols + k);
         const int s = FULL ? c : (H > 0 ? ld_nc_i32(p.eslot + k) : -1);
@@ -1537,6 +1542,7 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
           }
         }
       }
+      if (len > P)  // group-uniform: long rows only
       for (int kk = P + g; kk < len; kk += G) {
         const int64_t k = lo + kk;
         const int c = ld_nc_i32(p.cols + k);
