@@ -43,7 +43,7 @@ import datagen  # noqa: E402
 OPERATING_POINT = {
     "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
     # c2: every feature combined per thread block (asaga_combine_kernel), 46 workers per SM
-    "c2": dict(W=6808, gscale=0.045, bulk=0.0, split=0.0, repl=0, comb=1e-300),
+    "c2": dict(W=6808, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
     # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split)
     "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.3, repl=0, comb=0.0),
     "c4": dict(W=448, gscale=0.25, bulk=0.0, split=0.3, repl=0, comb=0.0),
