@@ -378,7 +378,8 @@ asaga_status configure_update(asaga_ctx* ctx) {
   if (lanes != 8 && lanes != 16 && lanes != 32)
     return fail(ctx, ASAGA_E_INVALID_ARG, "lanes_per_sample must be 0, 8, 16 or 32 (got %d)", lanes);
   int nr = 1;
-  while (nr < 8 && (double)(nr * lanes) < 2.0 * mean) nr *= 2;
+  // register chunks for about twice the mean row, but no more than the longest row needs
+  while (nr < 8 && (double)(nr * lanes) < 2.0 * mean && (int64_t)nr * lanes < ctx->max_row) nr *= 2;
   if ((int64_t)nr * lanes < ctx->max_row && ctx->max_row <= (int64_t)2 * nr * lanes && nr < 8) nr *= 2;
   int overflow = (int)std::max<int64_t>(0, ctx->max_row - (int64_t)nr * lanes);
   overflow = (overflow + 1) & ~1;  // keep every group's smem block 16-byte aligned
