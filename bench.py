@@ -395,8 +395,25 @@ def main():
 
     ttt = None
     if rank == 0 and not args.no_ttt:
+        # three runs with three sample streams (the paper averages 3 runs; SURVEY P14:
+        # judged on the mean, the worst reported)
         a.reload(indptr, indices, data, y)
-        ttt = time_to_target(a, p, stream, seed)
+        runs = [time_to_target(a, p, stream, seed + r) for r in range(3)]
+        if all(r is not None for r in runs):
+            ep = [r["epochs"] for r in runs]
+            sec = [r["seconds"] for r in runs]
+            ttt = dict(runs[0])
+            ttt["runs"] = [{"epochs": e, "seconds": s} for e, s in zip(ep, sec)]
+            if all(e is not None for e in ep):
+                ttt["epochs"] = float(np.mean(ep))
+                ttt["seconds"] = float(np.mean(sec))
+                ttt["worst_epochs"] = float(max(ep))
+                ttt["worst_seconds"] = float(max(sec))
+                ttt["within_1p5x_oracle_epochs"] = ttt["epochs"] <= 1.5 * ttt["oracle_epochs"]
+                ttt["worst_within_1p5x_oracle_epochs"] = max(ep) <= 1.5 * ttt["oracle_epochs"]
+            else:
+                ttt["epochs"] = ttt["seconds"] = None
+                ttt["within_1p5x_oracle_epochs"] = False
 
     if rank == 0:
         st = a.stats()
