@@ -277,7 +277,20 @@ def test_host_reload_async_double_buffered():
     with pytest.raises(m.AsagaError) as ei:
         a.objective()
     assert ei.value.name == "ASAGA_E_BAD_LABEL" and "row 17" in str(ei.value)
+    # a different shape is refused at the call; pageable numpy arrays work (blocking copy)
+    with pytest.raises(m.AsagaError) as ei:
+        a.reload_async(p.indptr[:-1].copy(), p.indices, p.data, p.y[:-1].copy())
+    assert ei.value.name == "ASAGA_E_INVALID_ARG"
+    a.reload_async(p.indptr, p.indices, p.data, p.y)
+    a.run(p.n, SEED)
+    r = oracle.sparse_saga(p, p.y, p.lam, g, SEED, p.n)
+    assert rel(a.get_state()[0], r.x) <= 1e-9
     a.close()
+    # before any successful ingest of the context's own shape it is the blocking reload
+    b = m.Asaga(pin(p.indptr), pin(p.indices), pin(p.data), pin(p.y), p.d, p.lam, g, deterministic=True)
+    b.reload_async(pin(q.indptr), pin(q.indices), pin(q.data), pin(q.y))
+    assert b.objective(np.zeros(p.d)) == pytest.approx(np.log(2.0), rel=1e-14)
+    b.close()
 
 
 # ---------------------------------------------------------------------- A9 objective / gradient
