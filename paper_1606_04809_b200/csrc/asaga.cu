@@ -509,10 +509,10 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   return ASAGA_OK;
 }
 
-// A0 + A1 on data already in device memory: rowptr/cols/y in the context's own
-// buffers, values in data_in (the caller's device array, or ctx->vals itself
-// after a host copy -- the fold is elementwise, so in place is safe).  Resets
-// the state to x = 0, alpha = 0, abar = 0, t = 0 (reading R1).
+// A0 + A1 on data already in device memory (the caller's device arrays, or the context's
+// own copy of host arrays): read-only validation and column counts; from here on the
+// kernels read these arrays.  Resets the state to x = 0, alpha = 0, abar = 0, t = 0
+// (reading R1).
 asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int32_t* indices_in,
                             const double* data_in, const double* y_in, bool guard) {
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;

@@ -3,11 +3,13 @@
 // Paper: Leblond, Pedregosa, Lacoste-Julien, "ASAGA: Asynchronous Parallel
 // SAGA", arXiv 1606.04809 (PAPER.md; cited "P:<line>").  Kernel map
 // (DESIGN.md "Kernels"):
-//   ingest_kernel        A0+A1: validate CSR, fold labels (a~ = b a), n_v, ||a_i||^2
-//   profile_kernel       A1: D_v = n/n_v, coordinate state {x, abar, D} init, Delta_r
+//   ingest_tile_kernel   A0+A1: validate the CSR (read-only), n_v, ||a_i||^2, longest row
+//   profile_kernel       A1: D_v = n/n_v, coordinate state {x, abar} init, Delta_r
+//   expand_d_kernel      A1: D per stored entry for the plain update kernel's row stream
 //   asaga_update_kernel  A2..A8: Philox sample -> row -> gather-dot -> sigma -> SAGA
 //                        correction -> red.global.add.f64 scatter (Alg. 2)
-//   margin_kernel        A9: m_i = a~_i.x, softplus(-m_i), sigma~_i (Section 4.1)
+//   asaga_combine_kernel A2..A8 with the hot features combined per thread block (R23)
+//   margin_*_kernel      A9: m_i = b_i a_i.x, softplus(-m_i), sigma~_i (Section 4.1)
 //   colseg_kernel        A9: sum_i sigma~_i a~_iv over fixed column segments (CSC)
 // No tensor cores: nothing here is a dense contraction.
 #pragma once
@@ -703,8 +705,9 @@ __global__ void hot_slot_kernel(const int32_t* __restrict__ flag, const int32_t*
 // A2..A8: the ASAGA update loop (Algorithm 2, + Section 4.2 l2 term).
 //
 // Worker w (a group of G lanes) processes t = t0 + w, t0 + w + W, ... (W workers
-// = samples in flight).  Per sample, with folded values a~ = b a and folded
-// memory alpha~_i = b_i alpha_i (exact: b = +-1):
+// = samples in flight).  Per sample, in the folded form a~ = b a (the label b_i comes
+// with the row and multiplies the margin and dalpha: exact, b = +-1) and folded memory
+// alpha~_i = b_i alpha_i:
 //   i      = Philox(seed, t)                               line 3 (sample first)
 //   x^, abar^ on S_i (.cg loads), D (L1)                   lines 5, 7
 //   m      = sum a~_k x^_{c_k}   (group shuffle reduce)
