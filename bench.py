@@ -478,12 +478,12 @@ def main():
                     "how": "asaga_reload_async from pinned host arrays (copy stream, two device "
                            "buffers: step k+1's H2D overlaps step k), run, objective, D2H of f; "
                            "wall clock over the K steps, L2 flushed between steps"},
-            # ours per step: ingest_init, ingest (for d <= 4096 its last block also runs the
-            # profile and the report; else profile + report kernels, and A9's dense copy of
-            # x), update, margin (its last block finishes f), + expand_d unless every
-            # feature is combined, + hot_flag and hot_slot when combining with d > 4096
-            # (CUB's scan kernels are library, not counted)
-            "gpu_launches": (4 + (0 if p.d <= 4096 else 3)
+            # ours per step: ingest_init (not for d <= 1024: the ingest initialises itself),
+            # ingest (for d <= 4096 its last block also runs the profile and the report; else
+            # profile + report kernels, and A9's dense copy of x), update, margin (its last
+            # block finishes f), + expand_d unless every feature is combined, + hot_flag and
+            # hot_slot when combining with d > 4096 (CUB's scan kernels are library)
+            "gpu_launches": (4 - (1 if p.d <= 1024 else 0) + (0 if p.d <= 4096 else 3)
                              + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) else 1)
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),

@@ -29,6 +29,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kColSeg = 2048;         // CSC entries per gradient segment
 constexpr int64_t kSmemHistMax = 48 * 1024;  // columns held in a shared histogram
+constexpr int64_t kSelfInitMaxD = 1024;      // the ingest initialises itself (no init launch)
 
 thread_local std::string g_thread_err = "no error";
 
@@ -121,6 +122,8 @@ struct asaga_ctx {
   double* xdense = nullptr; // d doubles: A9's dense copy of the current x (d > 4096)
   int obj_blocks = 0;
   bool margin_tiles = false;
+  bool self_init_ready = false;    // small d: the ingest kernel resets its own scratch
+  int32_t* ingest_part = nullptr;  // small d: per-block column counts (grid x d)
   int ingest_grid = 0;
   // CSC (built lazily)
   bool csc_built = false;
@@ -519,9 +522,15 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
   if (ctx->ov) CK(ctx, cudaMemsetAsync(ctx->ov, 0, 4 * sizeof(unsigned long long), ctx->stream));
-  ingest_init_kernel<<<grid_for(ctx, std::max(n, d), kBlock), kBlock, 0, ctx->stream>>>(
-      ctx->counts, d, ctx->alpha, n, scratch, ctx->flag);
-  CK(ctx, cudaGetLastError());
+  // small d: the ingest kernel initialises itself (IngestParams::self_init) once the state
+  // has been reset the first time; otherwise one init launch per ingest
+  const bool self_init = d <= kSelfInitMaxD;
+  if (!self_init || !ctx->self_init_ready) {
+    ingest_init_kernel<<<grid_for(ctx, std::max(n, d), kBlock), kBlock, 0, ctx->stream>>>(
+        ctx->counts, d, ctx->alpha, n, scratch, ctx->flag);
+    CK(ctx, cudaGetLastError());
+    ctx->self_init_ready = self_init;
+  }
   ctx->t = 0;
   ctx->snapshot_valid = false;
   if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
@@ -585,6 +594,10 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   // d <= 4096: the ingest's last block also runs A1's finish (D, state, Delta_r, the combine
   // hot set) and writes the validation report -- two launches fewer per ingest
   ip.fuse = d <= 4096 ? 1 : 0;
+  ip.self_init = self_init ? 1 : 0;
+  ip.alpha = ctx->alpha;
+  if (self_init && !ctx->ingest_part) TRY(dalloc(ctx, &ctx->ingest_part, (size_t)grid * d));
+  ip.part = ctx->ingest_part;
   ip.xa = ctx->xa;
   ip.S = ctx->S;
   ip.habar = ctx->habar;

@@ -212,6 +212,13 @@ struct IngestParams {
   int guard;
   int smem_hist;          // 1: per-block shared histogram of all d columns; 0: a per-block
                           // shared hash cache of kHashSlots columns (the popular ones claim it)
+  // self_init (fused, d <= kSelfInitMaxD): no ingest_init launch -- every block stores its
+  // histogram into part[block][d] (no atomics, no zeroed counts), zeroes alpha for its rows,
+  // and the last block sums the parts into counts, then (after the report) resets the error
+  // rows, the maxima and its ticket for the next ingest (set once at allocation)
+  int self_init;
+  int32_t* part;
+  double* alpha;
 };
 
 // ---------------------------------------------------------------------------
@@ -328,6 +335,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     const int64_t hi = row ? p.indptr[i + 1] : 0;
     const double b = row ? p.y[i] : 1.0;
     if (row && b != 1.0 && b != -1.0) atomicMin(&p.err_row[ERR_LABEL], (unsigned long long)i);
+    if (p.self_init && row) p.alpha[i] = 0.0;
     // bounds: every row inside [0, nnz], monotone, contiguous with the next row
     const int64_t next_lo = __shfl_down_sync(0xffffffffu, lo, 1);
     const bool bad_b = row && (lo < 0 || hi > p.nnz || hi < lo || (lane + 1 < nr && next_lo != hi));
@@ -510,7 +518,9 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     atomicMax(p.max_len, (unsigned long long)L);
   }
   __syncthreads();
-  if (p.smem_hist) {
+  if (p.self_init) {
+    for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) p.part[(int64_t)blockIdx.x * p.d + v] = hist[v];
+  } else if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
       if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
   } else {
@@ -525,11 +535,27 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     __syncthreads();
     if (is_last) {
       __threadfence();
+      if (p.self_init) {  // n_v = the sum of the blocks' parts, in block order
+        for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) {
+          int c = 0;
+          for (int bk = 0; bk < (int)gridDim.x; ++bk) c += __ldcg(p.part + (int64_t)bk * p.d + v);
+          p.counts[v] = c;
+        }
+        __syncthreads();
+      }
       profile_small_body(p.counts, p.xa, p.S, p.habar, p.D, (int)p.d, p.n, p.flag + 1, p.comb_dmax, p.max_h,
                          p.slot_of, p.hot_id, p.flag + 2);
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) report_body(p.err_row, p.flag, p.host_out, p.row_cap, p.hot_expected, p.guard);
+      if (threadIdx.x == 0) {
+        report_body(p.err_row, p.flag, p.host_out, p.row_cap, p.hot_expected, p.guard);
+        if (p.self_init) {  // ready for the next ingest
+          for (int q = 0; q < ERR_COUNT; ++q) p.err_row[q] = ~0ull;
+          p.err_row[ERR_COUNT] = 0ull;
+          p.err_row[ERR_COUNT + 1] = 0ull;
+          p.flag[4] = 0;
+        }
+      }
     }
   }
 }
