@@ -883,6 +883,49 @@ def test_ingest_errors_on_every_tile_path(L):
         assert "row 37" in str(ei.value), (fn.__name__, ei.value)
 
 
+@gpu
+def test_self_initialising_ingest_resets_between_ingests():
+    """d <= 1024: the ingest initialises itself (no init launch) and its last block resets
+    the error rows, maxima and ticket for the next ingest.  Alternate bad and good matrices
+    of one shape on one context, blocking and asynchronous: every bad one reports its own
+    first bad row, every good one ingests with exact n_v, L and the longest row, and runs
+    match the oracle."""
+    import torch
+
+    m = asaga_mod()
+    p = datagen.make("c2", n_rows=5000)
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, deterministic=True)
+    t = lambda arr: torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+    for k, bad_row in enumerate((13, 4000, 77)):
+        y = p.y.copy()
+        y[bad_row] = 3.0
+        with pytest.raises(m.AsagaError) as ei:
+            a.reload(p.indptr, p.indices, p.data, y)
+        assert ei.value.name == "ASAGA_E_BAD_LABEL" and f"row {bad_row}" in str(ei.value)
+        cols = p.indices.copy()
+        lo = p.indptr[bad_row + 1]
+        cols[lo], cols[lo + 1] = cols[lo + 1], cols[lo]  # row bad_row + 1 out of order
+        with pytest.raises(m.AsagaError) as ei:  # (after a failed ingest the asynchronous
+            a.reload_async(t(p.indptr), t(cols), t(p.data), t(p.y))  # reload is the blocking one)
+            a.objective()
+        assert ei.value.name == "ASAGA_E_BAD_CSR" and f"row {bad_row + 1}" in str(ei.value)
+        if k % 2 == 0:
+            a.reload(p.indptr, p.indices, p.data, p.y)
+        else:
+            a.reload_async(t(p.indptr), t(p.indices), t(p.data), t(p.y))
+        counts, D = a.profile()
+        ref = oracle.column_counts(p)
+        assert np.array_equal(counts.astype(np.int64), ref)
+        st = a.stats()
+        assert st["L"] == pytest.approx(oracle.lipschitz(p, p.lam), rel=1e-14)
+        assert st["max_row"] == p.row_lengths().max()
+        a.run(p.n, SEED)
+        r = oracle.sparse_saga(p, p.y, p.lam, g, SEED, p.n)
+        assert rel(a.get_state()[0], r.x) <= 1e-9
+    a.close()
+
+
 # ---------------------------------------------------------------------- degenerate and edge cases
 @gpu
 def test_degenerate_instances_match_the_oracle():
