@@ -926,6 +926,32 @@ def test_self_initialising_ingest_resets_between_ingests():
     a.close()
 
 
+@gpu
+def test_l2_persist_launch_path_is_bitwise_neutral():
+    """Option l2_persist_state only changes how the plain kernel is launched
+    (an L2 access-policy window): the deterministic iterate is bitwise the one without it,
+    and an asynchronous run keeps the quiescent identity."""
+    m = asaga_mod()
+    p = datagen.make("c3", n_rows=4000)
+    g = gamma_of(p)
+    runs = []
+    for persist in (False, True):
+        a = m.Asaga.from_problem(p, g, deterministic=True, l2_persist_state=persist)
+        a.run(2 * p.n, SEED)
+        runs.append(a.get_state()[:3])
+        a.close()
+    for u, v in zip(*runs):
+        assert np.array_equal(u, v)
+    a = m.Asaga.from_problem(p, g, concurrency=64, l2_persist_state=True)
+    a.run(2 * p.n, SEED)
+    import scipy.sparse
+
+    x, alpha, abar, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(abar, A.T @ alpha / p.n) <= 1e-10  # quiescent identity (no lost update)
+    a.close()
+
+
 # ---------------------------------------------------------------------- degenerate and edge cases
 @gpu
 def test_degenerate_instances_match_the_oracle():
