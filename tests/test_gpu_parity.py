@@ -777,6 +777,31 @@ def test_combine_clusters_and_write_through_keep_every_add(name, comb, cluster, 
     assert np.all(np.isfinite(x)) and a.objective() < np.log(2.0)
 
 
+@gpu
+@pytest.mark.parametrize("name,comb,max_blocks", [("c2s", 1e-300, 8), ("c3s", 0.3, 16)])
+def test_combine_max_blocks_packs_workers_and_keeps_every_add(name, comb, max_blocks):
+    """combine_max_blocks: the same samples in flight packed into fewer, fuller blocks --
+    the block count honours the cap, every t is processed once, the quiescent identity
+    holds and f falls below log 2."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 2 * p.n + 777
+    a = m.Asaga.from_problem(p, gamma_of(p) / 16, record_samples=True, concurrency=96,
+                             combine_min_freq=comb, combine_max_blocks=max_blocks)
+    st = a.stats()
+    assert 0 < st["combine_blocks"] <= max_blocks and st["combine_hot"] > 0
+    a.run(T, SEED)
+    ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
+    assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x)) and a.objective() < np.log(2.0)
+    a.close()
+
+
 def _mixed_rows_problem():
     """Short rows (mean ~6) with two 1,200-entry rows: most 32-row tiles take the ingest's
     staged path, the two holding the long rows take the flat path."""
