@@ -14,10 +14,12 @@ workload's convergent operating point (samples in flight W, step gamma =
 scale / (3L)) chosen from the sweeps in profiles/ (DESIGN.md "Operating
 point"); the line also reports time-to-1e-6 from x = 0 at that point.
 
-N > 1 ranks run independent lambda-sweep instances (lambda_r = 10^-r / n,
-SURVEY 8(e)): weak scaling, no collective on the data path.
+Workload: at N = 1 the default is c4, BASELINE.json's largest single-GPU configuration
+(URL-like, n = 2,396,130, d = 3,231,961).  N > 1 ranks run BASELINE config 5: c3's shape as
+independent lambda-sweep instances, lambda_r = 10^-(r+1) / n on rank r: weak
+scaling, no collective on the data path.  `--workload` overrides either.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4]
                     [--concurrency W] [--gamma-scale s] [--impl ours|reference]
 """
 from __future__ import annotations
@@ -36,6 +38,55 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import datagen  # noqa: E402
+
+# The same metric string in both arms (ours and --impl reference), so the driver can pair them.
+METRIC = "ASAGA updates/s"
+STEP = "one step = ingest A0-A1 + one epoch of n updates A2-A8 + objective A9"
+
+
+def default_workload(world: int) -> str:
+    """c4 at one GPU (BASELINE's largest single-GPU config); config 5 (c3 sweep) for N > 1."""
+    return "c4" if world <= 1 else "c3"
+
+
+def sweep_lambda(p, world: int, rank: int) -> float:
+    """lambda of this rank: 1/n at N = 1 (configs 1-4); config 5's 10^-(r+1)/n for N > 1."""
+    return p.lam if world <= 1 else p.lam * 10.0 ** (-(rank + 1))
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class pinned_core:
+    """Pin the calling thread (the oracle runs in it, through ctypes) to one host core for the
+    CPU baseline (`taskset -c 0`), restoring the previous affinity after."""
+
+    def __init__(self):
+        self.core = None
+        self.prev = None
+
+    def __enter__(self):
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = min(self.prev)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *a):
+        if self.prev is not None:
+            try:
+                os.sched_setaffinity(0, self.prev)
+            except OSError:
+                pass
 
 # Convergent operating points (W samples in flight, gamma scale vs 1/(3L), bulk-scatter
 # feature frequency) from tools/sweep.py on B200 (profiles/r01_operating_point.md):
@@ -70,7 +121,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    ap.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4"],
+                    help="default: c4 at N = 1, c3 (config 5 sweep) at N > 1")
     ap.add_argument("--concurrency", type=int, default=None, help="samples in flight")
     ap.add_argument("--gamma-scale", type=float, default=None)
     ap.add_argument("--l2-persist", type=int, default=None, help="override l2_persist_state (0/1)")
@@ -183,24 +235,37 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
-def cpu_baseline(p, gamma, seconds: float):
-    """The oracle (sequential fp64 Sparse SAGA, 1 host thread) on a bounded sample."""
+def cpu_baseline(p, lam, gamma, seconds: float):
+    """The oracle (sequential fp64 Sparse SAGA, 1 host thread pinned to one core) on a bounded
+    sample, plus its time to 1e-6: the oracle's epoch count from the golden file (written by
+    scripts/compute_fstar.py, f checked every n/10 updates) x n / the rate measured here --
+    extrapolated, not run to the end (SURVEY 8(d) allows it for the large configs)."""
     import oracle
 
     st = oracle.State(p.n, p.d)
     D = oracle.reweight(p.n, oracle.column_counts(p))
     probe = min(p.n, 20_000)
-    t0 = time.perf_counter()
-    oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, probe, st, D)
-    dt = time.perf_counter() - t0
-    T = max(probe, int(probe * seconds / max(dt, 1e-6)))
-    t0 = time.perf_counter()
-    oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, T, st, D)
-    dt = time.perf_counter() - t0
-    return {"value": T / dt, "unit": "updates/s", "cores": 1, "kind": "oracle",
-            "sample": f"{T} sequential updates (t={probe}..{probe + T - 1}) of {p.name} from x=0 "
-                      f"after a {probe}-update probe, gamma=1/(3L); {dt:.1f} s on 1 host thread "
-                      f"of {os.cpu_count()}"}
+    with pinned_core() as pin:
+        t0 = time.perf_counter()
+        oracle.sparse_saga(p, p.y, lam, gamma, datagen.SAMPLE_SEED, probe, st, D)
+        dt = time.perf_counter() - t0
+        T = max(probe, int(probe * seconds / max(dt, 1e-6)))
+        t0 = time.perf_counter()
+        oracle.sparse_saga(p, p.y, lam, gamma, datagen.SAMPLE_SEED, T, st, D)
+        dt = time.perf_counter() - t0
+    rate = T / dt
+    out = {"value": rate, "unit": "updates/s", "cores": 1, "kind": "oracle",
+           "cpu_model": cpu_model(), "host_threads": os.cpu_count(), "pinned_core": pin.core,
+           "sample": f"{T} sequential updates (t={probe}..{probe + T - 1}) of {p.name} from x=0 "
+                     f"after a {probe}-update probe, gamma=1/(3L); {dt:.1f} s on 1 host thread "
+                     f"(pinned to core {pin.core}) of {os.cpu_count()}"}
+    gold = load_json("tests", "golden", f"fstar_{p.name}.json")
+    if gold is not None and gold.get("sha256") == p.sha256() and lam == p.lam:
+        ep = gold["oracle_epochs_to_1e-6"]
+        out["time_to_1e-6"] = {"epochs": ep, "seconds": ep * p.n / rate,
+                               "how": "extrapolated: the oracle's epochs to 1e-6 (golden file, f every "
+                                      "n/10 updates) x n / the updates/s measured here"}
+    return out
 
 
 def run_reference(args, rank):
@@ -209,58 +274,85 @@ def run_reference(args, rank):
         return
     import oracle
 
-    p = datagen.make(args.workload)
-    gamma = 1.0 / (3.0 * oracle.lipschitz(p, p.lam))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    p = datagen.make(args.workload or default_workload(world))
+    lam = sweep_lambda(p, world, 0)
+    gamma = 1.0 / (3.0 * oracle.lipschitz(p, lam))
     st = oracle.State(p.n, p.d)
     D = oracle.reweight(p.n, oracle.column_counts(p))
     per_step = max(1000, min(p.n, 3_000_000 // max(args.steps + args.warmup, 1)))
-    for _ in range(args.warmup):
-        oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle.sparse_saga(p, p.y, p.lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
-    dt = time.perf_counter() - t0
+    with pinned_core() as pin:
+        for _ in range(args.warmup):
+            oracle.sparse_saga(p, p.y, lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.sparse_saga(p, p.y, lam, gamma, datagen.SAMPLE_SEED, per_step, st, D)
+        dt = time.perf_counter() - t0
     v = per_step * args.steps / dt
     sample = (f"{args.steps} steps x {per_step} sequential updates of {p.name} "
-              f"(a bounded sample of the n={p.n}-update epoch), 1 host thread of {os.cpu_count()}")
+              f"(a bounded sample of the n={p.n}-update epoch), 1 host thread (pinned to core "
+              f"{pin.core}) of {os.cpu_count()} ({cpu_model()}); the oracle is the reference arm "
+              f"(the paper's Scala code is not available)")
     print(json.dumps({
-        "impl": "reference", "metric": "ASAGA updates/s", "value": v, "unit": "updates/s",
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz},
+        "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz, "lambda": lam,
+                   "step": f"{per_step} oracle updates (a bounded sample of {STEP})"},
         "cpu_baseline": {"value": v, "unit": "updates/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "pinned_core": pin.core, "sample": sample},
         "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
 
-def time_to_target(a, p, stream, seed, tol=1e-6, max_epochs=40.0):
-    """From x = 0: epochs and update-kernel seconds until f - f* <= tol, f checked every
-    n/10 updates (reading R12; evaluation excluded). f* from the oracle's golden file."""
+def job_rate(local_ms: float, world: int, n: int, steps: int, device) -> tuple[float, float]:
+    """Whole-job throughput: every rank ran `steps` steps of n updates; the job's time is the
+    MAX over ranks of their timed totals (all-reduce MAX when world > 1).  Returns
+    (updates/s of all ranks together, the max total in ms)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(local_ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return world * n * steps / (ms / 1e3), ms
+
+
+def time_to_target(a, p, stream, seed, tol=1e-6, max_epochs=30):
+    """From x = 0: epochs and update-kernel seconds until f - f* <= tol, in the launch regime
+    `value` is measured in -- one launch per epoch, f checked after each (evaluation
+    excluded) -- against the oracle's epoch count at the same whole-epoch cadence (its
+    0.1-epoch count from the golden file, rounded up).  f* from the oracle's golden file."""
+    import math
+
     import torch
 
     gold = load_json("tests", "golden", f"fstar_{p.name}.json")
     if gold is None or gold.get("sha256") != p.sha256():
         return None
     fstar = gold["f_star"]
-    step = p.n // 10
+    oracle_ep = math.ceil(gold["oracle_epochs_to_1e-6"] - 1e-9)
     ms = 0.0
     a.set_state(np.zeros(p.d), np.zeros(p.n), np.zeros(p.d), 0)
-    for j in range(1, int(max_epochs * 10) + 1):
+    f = float("nan")
+    for j in range(1, max_epochs + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        a.run_async(step, seed)
+        a.run_async(p.n, seed)
         e1.record(stream)
         f = a.objective()
         ms += e0.elapsed_time(e1)
         if f - fstar <= tol:
-            return {"epochs": j / 10, "seconds": ms / 1e3, "tol": tol, "f_star": fstar,
-                    "oracle_epochs": gold["oracle_epochs_to_1e-6"],
-                    "within_1p5x_oracle_epochs": j / 10 <= 1.5 * gold["oracle_epochs_to_1e-6"]}
+            return {"epochs": j, "seconds": ms / 1e3, "tol": tol, "f_star": fstar,
+                    "launch": "one epoch per launch, f checked between launches",
+                    "oracle_epochs": oracle_ep, "oracle_epochs_tenths": gold["oracle_epochs_to_1e-6"],
+                    "within_1p5x_oracle_epochs": j <= 1.5 * oracle_ep}
         if not np.isfinite(f):
             break
-    return {"epochs": None, "seconds": None, "tol": tol, "f_star": fstar, "last_subopt": f - fstar}
+    return {"epochs": None, "seconds": None, "tol": tol, "f_star": fstar, "last_subopt": f - fstar,
+            "oracle_epochs": oracle_ep}
 
 
 def main():
@@ -279,14 +371,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1606_04809_b200 import Asaga
 
-    p = datagen.make(args.workload)
-    op = dict(OPERATING_POINT[args.workload])
+    workload = args.workload or default_workload(world)
+    p = datagen.make(workload)
+    op = dict(OPERATING_POINT[workload])
     if args.l2_persist is not None:
         op["persist"] = bool(args.l2_persist)
     W = args.concurrency if args.concurrency is not None else op["W"]
     gscale = args.gamma_scale if args.gamma_scale is not None else op["gscale"]
     bulk = op["bulk"]
-    lam = p.lam * (10.0 ** (-rank))  # rank 0: lambda = 1/n (the BASELINE config)
+    lam = sweep_lambda(p, world, rank)
     dev = torch.device("cuda", local)
     t = lambda arr: torch.from_numpy(arr).to(dev)
     indptr, indices, data, y = t(p.indptr), t(p.indices), t(p.data), t(p.y)
@@ -341,11 +434,7 @@ def main():
     ing_ms = [e[0].elapsed_time(e[1]) for e in all_evs]
     obj_ms = [e[2].elapsed_time(e[3]) for e in all_evs]
     f_final = float(f_dev.item())
-    tmax = torch.tensor([float(sum(step_ms))], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_ms_max = float(tmax.item())
-    value = world * p.n * args.steps / (total_ms_max / 1e3)
+    value, total_ms_max = job_rate(float(sum(step_ms)), world, p.n, args.steps, dev)
 
     # ---- e2e: the same step through the host-buffer C-ABI path (pinned host inputs; every
     # step's H2D copy and the D2H read of its f inside the timed region).  Pipelined as a
@@ -387,14 +476,10 @@ def main():
     e2e_run(args.warmup)
     e2e_total, f_host = e2e_run(args.steps)
     a.stats()  # a blocking call: the last asynchronous reload's validation
-    e2e_ms = [e2e_total]
-    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * p.n * args.steps / (float(e2e_t.item()) / 1e3)
+    e2e_value, _ = job_rate(e2e_total, world, p.n, args.steps, dev)
 
     ttt = None
-    if rank == 0 and not args.no_ttt:
+    if rank == 0 and not args.no_ttt and lam == p.lam:  # f* is known for lambda = 1/n
         # three runs with three sample streams (the paper averages 3 runs; SURVEY P14:
         # judged on the mean, the worst reported)
         a.reload(indptr, indices, data, y)
@@ -414,6 +499,38 @@ def main():
             else:
                 ttt["epochs"] = ttt["seconds"] = None
                 ttt["within_1p5x_oracle_epochs"] = False
+
+    # the max-throughput tau -- the update kernel alone at more samples in
+    # flight than the convergent point (one-epoch launches, no flush), and whether that
+    # point still meets the 1.5x budget (one sample stream)
+    maxtp = None
+    if rank == 0 and not args.no_ttt:
+        scan = []
+        for mult in (1, 2, 4, 8):
+            try:
+                a.set_concurrency(W * mult)
+            except Exception:
+                break
+            a.reload(indptr, indices, data, y)
+            a.run(p.n, seed)  # warm
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            a.run_async(p.n, seed)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            scan.append({"samples_in_flight": a.stats()["concurrency"],
+                         "updates_per_s": p.n / (e0.elapsed_time(e1) / 1e3)})
+        best = max(scan, key=lambda r: r["updates_per_s"])
+        maxtp = {"scan": scan, "samples_in_flight": best["samples_in_flight"],
+                 "updates_per_s": best["updates_per_s"], "gamma": gamma}
+        if lam == p.lam:
+            a.set_concurrency(best["samples_in_flight"])
+            r = time_to_target(a, p, stream, seed)
+            if r is not None:
+                maxtp["epochs_to_1e-6"] = r["epochs"]
+                maxtp["within_1p5x_oracle_epochs"] = (r["epochs"] is not None
+                                                     and r["epochs"] <= 1.5 * r["oracle_epochs"])
+        a.set_concurrency(W)
 
     if rank == 0:
         st = a.stats()
@@ -445,14 +562,15 @@ def main():
         else:
             hot, hot_ops = (mb.get("hot_pair") or {}).get("k10", {}).get("updates_per_s_per_pair"), "pair load + two REDs per update"
         out = {
-            "metric": "ASAGA updates/s (one step = ingest A0-A1 + one epoch of updates A2-A8 + objective A9)",
+            "metric": METRIC,
             "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (datagen recipe, DESIGN.md 'Input recipe')",
-            "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz,
+            "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz, "step": STEP,
                        "samples_in_flight": st["concurrency"], "lanes_per_sample": st["lanes_per_sample"],
-                       "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale, "lambda": "10^-rank / n",
+                       "gamma": gamma, "gamma_scale_vs_1_over_3L": gscale,
+                       "lambda": lam if world == 1 else "10^-(rank+1) / n (BASELINE config 5)",
                        "bulk_scatter_min_freq": bulk, "hot_split_min_freq": op["split"],
                        "smem_replica_refresh": op["repl"], "combine_min_freq": op["comb"],
                        "combine_hot_features": st["combine_hot"],
@@ -462,6 +580,7 @@ def main():
                              "objective_A9": float(np.mean(obj_ms))},
             "update_kernel_updates_per_s": ups,
             "time_to_1e-6": ttt,
+            "max_throughput_point": maxtp,
             "f_after_step": f_final,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": None,
@@ -490,9 +609,14 @@ def main():
         }
         tr = load_json("profiles", "traffic.json") or {}
         if p.name in tr:
+            # ncu cannot run inside the timed bench: the DRAM bytes of one launch of the same
+            # kernel at the same operating point, from the committed ncu capture
             out["roofline"]["traffic"] = tr[p.name]
+            out["roofline"]["traffic_source"] = ("stored: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                                 "update launch (one epoch) from an ncu --set full capture "
+                                                 "(profiles/traffic.json), not measured in this run")
         if not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(p, 1.0 / (3.0 * L), args.cpu_seconds)
+            out["cpu_baseline"] = cpu_baseline(p, lam, 1.0 / (3.0 * L), args.cpu_seconds)
         print(json.dumps(out))
     a.close()
     if world > 1:

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define ASAGA_ABI_VERSION 1
+#define ASAGA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define ASAGA_API __attribute__((visibility("default")))
@@ -185,8 +185,10 @@ ASAGA_API asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, cons
 
 /* As asaga_init, but A's three arrays and y are DEVICE pointers (e.g. torch
  * tensors).  They are BORROWED, not copied: the context reads them (never writes)
- * until the next reload or asaga_destroy, so the caller keeps them allocated and
- * unchanged until then.  Validation runs on the device.  (The labels are applied per
+ * until the work enqueued before the next reload has completed on the context's stream
+ * (asaga_stream), or asaga_destroy, so the caller keeps them allocated and unchanged
+ * until then (a reload returns before earlier asaga_run_async work is done: order the
+ * arrays' release after an event recorded on asaga_stream, as the Python binding does).  Validation runs on the device.  (The labels are applied per
  * sample and per row in the kernels -- a~_i = b_i a_i is never materialised -- so an
  * ingest moves the matrix once, read-only.) */
 ASAGA_API asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* A_dev,
@@ -198,7 +200,12 @@ ASAGA_API asaga_status asaga_init_device(asaga_ctx** out, const asaga_csr_view* 
  * context's own device arrays) or DEVICE arrays (asaga_reload_device; borrowed as
  * in asaga_init_device, in place of the previous ones).  Runs A0-A1 again and resets the state to
  * x = 0, alpha = 0, abar = 0, t = 0.  Errors as asaga_init; a different shape
- * gives ASAGA_E_INVALID_ARG.  Blocking (the validation result is read back). */
+ * gives ASAGA_E_INVALID_ARG.  Blocking (the validation result is read back).
+ * REJECTED DATA: after a reload (blocking or asynchronous) fails validation, every call
+ * that would launch a kernel on the matrix -- asaga_run[_async], asaga_objective[_device],
+ * asaga_full_grad, asaga_partial_obj_grad, asaga_snapshot -- returns ASAGA_E_STATE until
+ * a reload succeeds, and the device-side run guard is closed, so no update kernel reads
+ * the rejected arrays. */
 ASAGA_API asaga_status asaga_reload(asaga_ctx* ctx, const asaga_csr_view* A, const double* y);
 ASAGA_API asaga_status asaga_reload_device(asaga_ctx* ctx, const asaga_csr_view* A_dev,
                                            const double* y_dev);
@@ -276,6 +283,14 @@ ASAGA_API asaga_status asaga_get_profile(asaga_ctx* ctx, int32_t* counts, double
 /* Per-row visit counts (HOST int32[n]) since init or the last reset; needs
  * options.record_samples = 1, else ASAGA_E_STATE. reset != 0 zeroes them after the copy. */
 ASAGA_API asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset);
+
+/* Checksum of the processed sample stream itself (the t -> i_t map, not only the per-row
+ * histogram): *hash = sum over every processed update t of mix(t, i_t) mod
+ * 2^64, mix(t, i) = splitmix64's finaliser applied to t * 0x9E3779B97F4A7C15 + i (z ^= z>>30;
+ * z *= 0xBF58476D1CE4E5B9; z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31), since init /
+ * the last ingest / the last reset.  Sampling rule: Alg. 2 line 3 under reading
+ * R2.  Needs options.record_samples = 1, else ASAGA_E_STATE.  reset != 0 zeroes it. */
+ASAGA_API asaga_status asaga_get_sample_hash(asaga_ctx* ctx, uint64_t* hash, int reset);
 
 /* Select the update rule (asaga_algorithm).  Switching to HOGWILD zeroes alpha and abar
  * (its memory is identically 0); switching to KROMAGNON requires asaga_snapshot()

@@ -75,9 +75,6 @@ def _load():
             "oracle_full_grad": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, f64, _F64P, _F64P]),
             "oracle_sparse_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                           u64, u64, u64, _F64P, _F64P, _F64P]),
-            "oracle_sparse_saga_trace": (i64, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64,
-                                               f64, u64, u64, u64, i64, _F64P, _F64P, _F64P,
-                                               _F64P]),
             "oracle_delayed_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                            u64, u64, u64, i64, _F64P, _F64P, _F64P]),
             "oracle_hogwild": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
@@ -225,25 +222,6 @@ def saga_step(A, y, lam: float, gamma: float, i: int, state: State, D: np.ndarra
                              _p(y, _F64P), _p(D, _F64P), lam, gamma, i, _p(state.x, _F64P),
                              _p(state.alpha, _F64P), _p(state.alpha_bar, _F64P), _p(u, _F64P))
     return state
-
-
-def sparse_saga_trace(A, y, lam, gamma, seed, eval_every: int, n_evals: int,
-                      state: State | None = None, D=None):
-    """Sparse SAGA with f evaluated every ``eval_every`` updates. Returns (state, f_trace)."""
-    n, d, indptr, indices, data = _csr(A)
-    y = np.ascontiguousarray(y, dtype=np.float64)
-    if state is None:
-        state = State(n, d)
-    if D is None:
-        D = reweight(n, column_counts(A))
-    f = np.empty(n_evals, dtype=np.float64)
-    _load().oracle_sparse_saga_trace(n, d, _p(indptr, _I64P), _p(indices, _I32P),
-                                     _p(data, _F64P), _p(y, _F64P), _p(D, _F64P), lam, gamma,
-                                     seed, state.t, eval_every, n_evals, _p(state.x, _F64P),
-                                     _p(state.alpha, _F64P), _p(state.alpha_bar, _F64P),
-                                     _p(f, _F64P))
-    state.t += eval_every * n_evals
-    return state, f
 
 
 def delayed_saga(A, y, lam, gamma, seed, T: int, tau: int, state: State | None = None, D=None):

@@ -203,23 +203,6 @@ void oracle_sparse_saga(int64_t n, int64_t d, const int64_t* indptr,
   free(u);
 }
 
-/* Same run, with the objective evaluated every eval_every updates (reading R12),
- * written to f_trace[0..n_evals-1]; f_trace[j] is f after (j+1)*eval_every
- * updates.  Returns the number of evaluations written. */
-int64_t oracle_sparse_saga_trace(int64_t n, int64_t d, const int64_t* indptr,
-                                 const int32_t* indices, const double* data,
-                                 const double* y, const double* D, double lambda,
-                                 double gamma, uint64_t seed, uint64_t t0,
-                                 uint64_t eval_every, int64_t n_evals, double* x,
-                                 double* alpha, double* alpha_bar, double* f_trace) {
-  for (int64_t j = 0; j < n_evals; ++j) {
-    oracle_sparse_saga(n, d, indptr, indices, data, y, D, lambda, gamma, seed,
-                       t0 + (uint64_t)j * eval_every, eval_every, x, alpha, alpha_bar);
-    f_trace[j] = oracle_objective(n, d, indptr, indices, data, y, lambda, x);
-  }
-  return n_evals;
-}
-
 /* ------------------------------------------------------------------------ */
 /* Bounded-delay Sparse SAGA (NEXT-1 tool, Assumption 1 P:316-322 taken at its
  * bound): update t reads x, alpha_i and abar as they stand after updates

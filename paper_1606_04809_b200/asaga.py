@@ -94,6 +94,7 @@ ABI_FUNCTIONS = {
                                        ctypes.c_void_p, _U64P]),
     "asaga_get_profile": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "asaga_get_sample_counts": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "asaga_get_sample_hash": (ctypes.c_int, [ctypes.c_void_p, _U64P, ctypes.c_int]),
     "asaga_set_gamma": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_double]),
     "asaga_set_algorithm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "asaga_snapshot": (ctypes.c_int, [ctypes.c_void_p]),
@@ -224,8 +225,9 @@ class Asaga:
     # ------------------------------------------------------------------ lifecycle
     def close(self):
         if getattr(self, "_h", None):
-            _lib.asaga_destroy(self._h)
+            _lib.asaga_destroy(self._h)  # synchronises the context's streams
             self._h = None
+            self._retired = []
 
     def __del__(self):
         try:
@@ -250,7 +252,7 @@ class Asaga:
                        _ptr(indices), _ptr(data))
         fn = _lib.asaga_reload_device if dev else _lib.asaga_reload
         _check(fn(self._h, ctypes.byref(view), _ptr(y)), self._h)
-        self._keep = (indptr, indices, data, y) if dev else None  # borrowed device arrays
+        self._borrow((indptr, indices, data, y) if dev else None)  # borrowed device arrays
 
     def reload_async(self, indptr, indices, data, y) -> None:
         """Non-blocking re-ingest; validation is reported by the next blocking call.
@@ -264,12 +266,30 @@ class Asaga:
             data, y = _host(data, np.float64), _host(y, np.float64)
         view = CsrView(int(indptr.shape[0]) - 1, self.d, int(indices.shape[0]), _ptr(indptr),
                        _ptr(indices), _ptr(data))
-        if dev:
-            self._keep = (indptr, indices, data, y)
-        else:
-            self._keep_host = (indptr, indices, data, y)
         fn = _lib.asaga_reload_device_async if dev else _lib.asaga_reload_async
         _check(fn(self._h, ctypes.byref(view), _ptr(y)), self._h)
+        # (references replaced only after the call: it first waits for the previous host
+        # copy, which reads the previous host arrays)
+        if dev:
+            self._borrow((indptr, indices, data, y))
+        else:
+            self._keep_host = (indptr, indices, data, y)
+
+    def _borrow(self, arrays) -> None:
+        """Replace the borrowed device arrays.  Work already enqueued on the context's stream
+        (e.g. an earlier run_async) may still read the previous ones, and torch's caching
+        allocator does not know that stream: keep them alive, with an event recorded on the
+        context's stream now, until that event has completed (checked at every reload; all
+        released at close, which synchronises the stream)."""
+        old = getattr(self, "_keep", None)
+        if old is not None and self._h:
+            import torch
+
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.ExternalStream(self.stream, device=old[0].device))
+            self._retired = [(e, k) for e, k in getattr(self, "_retired", []) if not e.query()]
+            self._retired.append((ev, old))
+        self._keep = arrays
 
     def run(self, n_updates: int, seed: int) -> None:
         _check(_lib.asaga_run(self._h, int(n_updates), int(seed)), self._h)
@@ -321,6 +341,12 @@ class Asaga:
         v = np.empty(self.n, dtype=np.int32)
         _check(_lib.asaga_get_sample_counts(self._h, _ptr(v), int(reset)), self._h)
         return v
+
+    def sample_hash(self, reset: bool = False) -> int:
+        """sum over processed t of mix(t, i_t) mod 2^64 (include/asaga.h asaga_get_sample_hash)."""
+        h = ctypes.c_uint64()
+        _check(_lib.asaga_get_sample_hash(self._h, ctypes.byref(h), int(reset)), self._h)
+        return h.value
 
     def set_gamma(self, gamma: float) -> None:
         _check(_lib.asaga_set_gamma(self._h, float(gamma)), self._h)

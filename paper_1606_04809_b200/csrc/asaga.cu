@@ -94,6 +94,12 @@ struct asaga_ctx {
   unsigned long long* h_ing_dev = nullptr;  // ... its device address
   cudaEvent_t ev_ing = nullptr;         // recorded after the ingest's readback copies
   bool ing_pending = false;             // an asynchronous reload awaits ingest_resolve
+  // the arrays the kernels read passed validation (false from an ingest's enqueue until its
+  // resolve succeeds): every entry point that launches a kernel on the matrix refuses to
+  // run on rejected data (ASAGA_E_STATE) until a reload succeeds
+  bool data_valid = false;
+  std::string reject_msg;               // why the last ingest was rejected
+  cudaEvent_t ev_part = nullptr;        // asaga_partial_obj_grad: caller stream <-> ctx stream
   bool ing_fused = false;               // the last ingest launch ran A1's finish and the report
   long long shape_key[6] = {0, 0, 0, 0, 0, 0};
   int32_t* comb_flag = nullptr;  // d scratch: hot flags, then their exclusive scan
@@ -106,6 +112,7 @@ struct asaga_ctx {
   double* alpha = nullptr;  // folded alpha~ = b alpha
   int32_t* counts = nullptr;
   int32_t* visits = nullptr;
+  unsigned long long* shash = nullptr;  // record_samples: sum of mix(t, i_t)
   unsigned long long* ov = nullptr;  // overlap instrumentation (4 counters)
   int algorithm = ASAGA_ALG_ASAGA;
   bool snapshot_valid = false;       // KROMAGNON: alpha / abar hold a snapshot
@@ -492,7 +499,10 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   TRY(dalloc(ctx, &ctx->scal, 4));
   TRY(dalloc(ctx, &ctx->flag, 8));  // [0] non-finite, [1] max n_v, [2] hot count, [3] run guard, [4] ingest blocks, [5] objective blocks
   TRY(dalloc(ctx, &ctx->scratch, ERR_COUNT + 3));  // err rows, max ||a||^2, max row, comm passes
-  if (ctx->record) TRY(dalloc(ctx, &ctx->visits, n));
+  if (ctx->record) {
+    TRY(dalloc(ctx, &ctx->visits, n));
+    TRY(dalloc(ctx, &ctx->shash, 1));
+  }
   if (ctx->ov_every > 0) TRY(dalloc(ctx, &ctx->ov, 4));
   CK(ctx, cudaHostAlloc(&ctx->h_ing, sizeof(unsigned long long) * (ERR_COUNT + 3), cudaHostAllocMapped));
   CK(ctx, cudaHostGetDevicePointer(&ctx->h_ing_dev, ctx->h_ing, 0));
@@ -521,6 +531,7 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   const int64_t n = ctx->n, d = ctx->d, nnz = ctx->nnz;
   unsigned long long* scratch = ctx->scratch;
   if (ctx->visits) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * n, ctx->stream));
+  if (ctx->shash) CK(ctx, cudaMemsetAsync(ctx->shash, 0, sizeof(unsigned long long), ctx->stream));
   if (ctx->ov) CK(ctx, cudaMemsetAsync(ctx->ov, 0, 4 * sizeof(unsigned long long), ctx->stream));
   // small d: the ingest kernel initialises itself (IngestParams::self_init) once the state
   // has been reset the first time; otherwise one init launch per ingest
@@ -533,6 +544,7 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   }
   ctx->t = 0;
   ctx->snapshot_valid = false;
+  ctx->data_valid = false;
   if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
     CK(ctx, cudaStreamSynchronize(ctx->stream));
     dfree(ctx, &ctx->csc_rows);
@@ -658,7 +670,30 @@ asaga_status enqueue_expand(asaga_ctx* ctx) {
 
 // Read back an enqueued ingest's validation: errors (with the first bad row), L, the
 // longest row, Delta_r and the combine hot count.  Blocks on the ingest's event only.
+asaga_status ingest_resolve_impl(asaga_ctx* ctx);
 asaga_status ingest_resolve(asaga_ctx* ctx) {
+  const asaga_status s = ingest_resolve_impl(ctx);
+  ctx->data_valid = s == ASAGA_OK;
+  if (s != ASAGA_OK) ctx->reject_msg = ctx->err;
+  if (s != ASAGA_OK && s != ASAGA_E_CUDA && s != ASAGA_E_OOM) {
+    // rejected data: close the device-side run guard as well, so no update kernel already
+    // or later enqueued (run_async) reads it, whatever the last good ingest left there
+    set_flag_kernel<<<1, 1, 0, ctx->stream>>>(ctx->flag + 3, 0);
+    (void)cudaGetLastError();
+  }
+  return s;
+}
+
+// Refuse kernels on a matrix that failed validation (the context still points at
+// the rejected arrays) -- unless an asynchronous reload is pending, whose run guard decides
+// on the device.
+asaga_status require_data(asaga_ctx* ctx) {
+  if (ctx->data_valid || ctx->ing_pending) return ASAGA_OK;
+  return fail(ctx, ASAGA_E_STATE, "no valid data: the last reload failed validation (%s); reload valid data first",
+              ctx->reject_msg.c_str());
+}
+
+asaga_status ingest_resolve_impl(asaga_ctx* ctx) {
   CK(ctx, cudaEventSynchronize(ctx->ev_ing));
   ctx->ing_pending = false;
   const volatile unsigned long long* hv = ctx->h_ing;  // written by the device (mapped)
@@ -833,6 +868,7 @@ asaga_status finish_init(asaga_ctx** out, asaga_ctx* ctx, asaga_status s) {
 }
 
 asaga_status ensure_csc(asaga_ctx* ctx) {
+  TRY(require_data(ctx));
   if (ctx->csc_built) return ASAGA_OK;
   const int64_t d = ctx->d, nnz = ctx->nnz, n = ctx->n;
   cudaStream_t s = ctx->stream;
@@ -914,6 +950,7 @@ asaga_status ensure_csc(asaga_ctx* ctx) {
 // (element stride xs: 1 for a dense vector, 2 for the {x, abar} pairs).
 asaga_status enqueue_objective(asaga_ctx* ctx, const double* x_dev, int xs, double* f_dev,
                                double* loss_sum_dev, bool want_sig, cudaStream_t s) {
+  TRY(require_data(ctx));
   double* sig = want_sig ? ctx->sig : nullptr;
   // the margin kernel's last block also finishes f (ticket in flag[5], reset by that block)
   const ObjFinish fin{ctx->flag + 5, ctx->n, ctx->lambda, f_dev, loss_sum_dev};
@@ -962,6 +999,7 @@ const double* current_x(asaga_ctx* ctx, int* xs, cudaStream_t s) {
 }
 
 asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool timed) {
+  TRY(require_data(ctx));
   if (n_updates == 0) return ASAGA_OK;
   if (ctx->algorithm == ASAGA_ALG_KROMAGNON && !ctx->snapshot_valid)
     return fail(ctx, ASAGA_E_STATE, "KROMAGNON needs asaga_snapshot() before asaga_run");
@@ -977,6 +1015,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.habar = ctx->habar;
   p.alpha = ctx->alpha;
   p.visits = ctx->visits;
+  p.shash = ctx->shash;
   p.ov = ctx->ov;
   p.frozen = ctx->algorithm != ASAGA_ALG_ASAGA ? 1 : 0;
   p.repl_d = use_replica(ctx) ? (int)ctx->d : 0;
@@ -1294,8 +1333,20 @@ asaga_status asaga_partial_obj_grad(asaga_ctx* ctx, const double* x_dev, double*
   TRY(resolve_pending(ctx));  // an asynchronous reload's validation
   TRY(ensure_csc(ctx));
   cudaStream_t s = stream ? (cudaStream_t)stream : ctx->stream;
+  // the partial shares the context's A9 scratch (finish ticket, block partials, sigma,
+  // segment sums) with asaga_objective on ctx->stream: order the two streams both ways
+  const bool other = s != ctx->stream;
+  if (other) {
+    if (!ctx->ev_part) CK(ctx, cudaEventCreateWithFlags(&ctx->ev_part, cudaEventDisableTiming));
+    CK(ctx, cudaEventRecord(ctx->ev_part, ctx->stream));
+    CK(ctx, cudaStreamWaitEvent(s, ctx->ev_part, 0));
+  }
   TRY(enqueue_objective(ctx, x_dev, 1, nullptr, out_dev + ctx->d, true, s));
   TRY(enqueue_gradient(ctx, x_dev, 1, out_dev, 0, s));
+  if (other) {
+    CK(ctx, cudaEventRecord(ctx->ev_part, s));
+    CK(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_part, 0));
+  }
   return ASAGA_OK;
 }
 
@@ -1367,6 +1418,19 @@ asaga_status asaga_get_sample_counts(asaga_ctx* ctx, int32_t* visits, int reset)
   CK(ctx, cudaMemcpyAsync(visits, ctx->visits, sizeof(int32_t) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
   if (reset) CK(ctx, cudaMemsetAsync(ctx->visits, 0, sizeof(int32_t) * ctx->n, ctx->stream));
   CK(ctx, cudaStreamSynchronize(ctx->stream));
+  return ASAGA_OK;
+}
+
+asaga_status asaga_get_sample_hash(asaga_ctx* ctx, uint64_t* hash, int reset) {
+  if (!ctx || !hash) return fail(ctx, ASAGA_E_INVALID_ARG, "NULL argument");
+  if (!ctx->shash) return fail(ctx, ASAGA_E_STATE, "context was created without record_samples");
+  CK(ctx, cudaSetDevice(ctx->device));
+  TRY(resolve_pending(ctx));  // an asynchronous reload's validation
+  unsigned long long h = 0;
+  CK(ctx, cudaMemcpyAsync(&h, ctx->shash, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  if (reset) CK(ctx, cudaMemsetAsync(ctx->shash, 0, sizeof(h), ctx->stream));
+  CK(ctx, cudaStreamSynchronize(ctx->stream));
+  *hash = (uint64_t)h;
   return ASAGA_OK;
 }
 
@@ -1545,6 +1609,7 @@ void asaga_destroy(asaga_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev_ing) cudaEventDestroy(ctx->ev_ing);
+  if (ctx->ev_part) cudaEventDestroy(ctx->ev_part);
   if (ctx->h_ing) cudaFreeHost(ctx->h_ing);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   for (auto& h : ctx->hs) {

@@ -47,6 +47,18 @@ __device__ __forceinline__ uint2 philox_lo64(uint64_t t, uint64_t seed) {
   return make_uint2(c0, c1);
 }
 
+// Sample-stream checksum (record_samples): sum over processed t of
+// mix(t, i_t) mod 2^64 (a splitmix64 finaliser of t * phi + i_t): it holds the t -> i_t map
+// itself, not just the per-row visit histogram.  The tests recompute it from the oracle's
+// stream (their own copy of this public mixing function: test infrastructure, no method
+// arithmetic).
+__device__ __forceinline__ unsigned long long sample_mix(uint64_t t, int64_t i) {
+  uint64_t z = t * 0x9E3779B97F4A7C15ull + (uint64_t)i;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
 // i_t = floor(r * n / 2^64), r = (w1 << 32) | w0 (reading R2).
 __device__ __forceinline__ int64_t sample_row(uint64_t seed, uint64_t t, uint64_t n) {
   const uint2 w = philox_lo64(t, seed);
@@ -161,7 +173,8 @@ __device__ __forceinline__ double sigma_folded(double m) {
   rc = fma(rc, e, rc);
   e = fma(-dd, rc, 1.0);
   rc = fma(rc, e, rc);
-  return m >= 0.0 ? -t * rc : -rc;
+  // a NaN margin stays NaN (fmax above would drop it), so divergence reaches alpha and abar too
+  return m != m ? m : (m >= 0.0 ? -t * rc : -rc);
 }
 
 // Test hook (asaga_debug_sigma): sigma_folded over a device array.
@@ -761,6 +774,7 @@ struct UpdateParams {
   double* habar;        // abar_v of hot-split features (entries with dv < 0)
   double* alpha;        // folded alpha~
   int32_t* visits;      // NULL unless record_samples
+  unsigned long long* shash;  // NULL unless record_samples: sum over processed t of mix(t, i_t)
   unsigned long long* ov;  // NULL, or overlap instrumentation (NEXT-1, App. D):
                            // [0] sparse global progress counter (+100 per 100 local samples),
                            // [1] sum and [2] count of per-sample overlap estimates, [3] max
@@ -935,6 +949,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   }
 
   unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
+  unsigned long long shash = 0;
   int ov_local = 0, ov_iter = 0;
   while (true) {
     // overlap estimate (App. D): progress counter at the read and after the write
@@ -1101,7 +1116,10 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       } else {
         st_cg(p.alpha + i, ai + da);
       }
-      if (p.visits) atomicAdd(p.visits + i, 1);
+      if (p.visits) {
+        atomicAdd(p.visits + i, 1);
+        shash += sample_mix(t, i);
+      }
       if (p.ov != nullptr) {
         if (++ov_local == 100) {  // sparse counter: one +100 per 100 local updates
           atomicAdd(p.ov, 100ull);
@@ -1142,6 +1160,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   }
   cp_async_wait_all();
   if (MODE == 2) bulk_wait_all();
+  if (p.visits && g == 0) atomicAdd(p.shash, shash);
   if (p.ov != nullptr && g == 0 && ov_cnt > 0) {
     atomicAdd(p.ov + 1, ov_sum);
     atomicAdd(p.ov + 2, ov_cnt);
@@ -1174,8 +1193,11 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 // (the comm warp flushes pend after the block's workers finish), so the quiescent
 // identity abar = (1/n) sum_i alpha_i a_i holds as in the plain kernel.
 // Worker w = blockIdx.x * nwb + (thread / G), processes t = t0 + w + kW as in
-// asaga_update_kernel (same t -> worker map).  The next sample's alpha_i is loaded
-// one sample early, with its row.
+// asaga_update_kernel (same t -> worker map).  alpha_i is copied with its row, KS = 3
+// samples ahead of its use (about 3W updates before this worker adds to it): the read of
+// the memory alpha^_i is inconsistent by that bounded window, counted in
+// DESIGN.md reading R23 (a repeat of i within ~3W updates, probability ~3W/n, sees the
+// older alpha^_i; the atomic add still applies every dalpha exactly once).
 template <int G, int NR, bool FULL>
 struct CombSmem {
   static constexpr int P = NR * G;
@@ -1478,6 +1500,7 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
     start_sync();
     if (active) {
     unsigned long long ov_sum = 0, ov_cnt = 0, ov_max = 0;
+    unsigned long long shash = 0;
     int ov_local = 0, ov_iter = 0;
     int stage = 0, rs = 0;  // row stage and bounds-ring slot of sample m
     // this worker's samples: t_first + mW < tend  (32-bit counts from here on)
@@ -1589,7 +1612,10 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
       }
       if (g == 0) {
         if (!p.frozen) red_add(p.alpha + i, da);
-        if (p.visits) atomicAdd(p.visits + i, 1);
+        if (p.visits) {
+          atomicAdd(p.visits + i, 1);
+          shash += sample_mix(t, i);
+        }
         if (p.ov != nullptr) {
           if (++ov_local == 100) {
             atomicAdd(p.ov, 100ull);
@@ -1626,6 +1652,7 @@ __global__ void __launch_bounds__(comb_block_threads(NR), 1) asaga_combine_kerne
       rs = (rs + 1 == SM::NB) ? 0 : rs + 1;
     }
     cp_async_wait_all();
+    if (p.visits && g == 0) atomicAdd(p.shash, shash);
     if (p.ov != nullptr && g == 0 && ov_cnt > 0) {
       atomicAdd(p.ov + 1, ov_sum);
       atomicAdd(p.ov + 2, ov_cnt);

@@ -64,7 +64,11 @@ class ShardedObjective:
         self.out = torch.zeros(self.d + 1, dtype=torch.float64, device=self.device)
 
     def __call__(self, x):
-        """x: float64 tensor of d on self.device (rank 0's value is used). Returns (f, grad)."""
+        """x: float64 tensor of d on self.device (rank 0's value is used).  Returns (f, grad)
+        as tensors on self.device (f 0-dimensional): no host round trip.  Everything is
+        ordered on torch's current stream -- the broadcast, the partial (launched on that
+        stream) and the all-reduce (NCCL is stream-ordered) -- so nothing synchronises the
+        host; read f with float(f) when it is needed there."""
         import torch
         import torch.distributed as dist
 
@@ -72,10 +76,8 @@ class ShardedObjective:
         if dist.is_initialized():
             dist.broadcast(x, src=0, group=self.group)
         self.partial(x, self.out)
-        if self.device.type == "cuda":
-            torch.cuda.current_stream(self.device).synchronize()
         if dist.is_initialized():
             dist.all_reduce(self.out, op=dist.ReduceOp.SUM, group=self.group)
-        f = float(self.out[self.d].item()) / self.n + 0.5 * self.lam * float(torch.dot(x, x).item())
+        f = self.out[self.d] / self.n + 0.5 * self.lam * torch.dot(x, x)
         g = self.out[: self.d] / self.n + self.lam * x
         return f, g

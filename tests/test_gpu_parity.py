@@ -20,6 +20,20 @@ def rel(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
+def sample_hash_ref(seed, t0, T, n):
+    """sum over t in [t0, t0+T) of mix(t, i_t) mod 2^64 for the ORACLE's sample stream, mix =
+    the splitmix64 finaliser of t * 0x9E3779B97F4A7C15 + i (include/asaga.h
+    asaga_get_sample_hash): equal sums mean the GPU processed the same (t, i_t) pairs."""
+    i = oracle.sample_stream(seed, t0, T, n).astype(np.uint64)
+    t = np.arange(t0, t0 + T, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = t * np.uint64(0x9E3779B97F4A7C15) + i
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+        return int(z.sum(dtype=np.uint64))
+
+
 def asaga_mod():
     import paper_1606_04809_b200 as m
 
@@ -105,6 +119,12 @@ def test_sigma_device_function_accuracy():
     order = np.argsort(z, kind="stable")  # monotone up to rounding (a few ulp)
     g = got[order]
     assert np.all(np.diff(g) >= -4 * np.spacing(np.abs(g[1:])))
+    # a NaN margin propagates (a diverged iterate must reach alpha and abar)
+    zn = torch.tensor([np.nan, -np.nan, np.inf, -np.inf], dtype=torch.float64, device="cuda")
+    on = torch.empty_like(zn)
+    m.debug_sigma(zn, on)
+    on = on.cpu().numpy()
+    assert np.isnan(on[0]) and np.isnan(on[1]) and -1e-300 <= on[2] <= 0.0 and on[3] == -1.0
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
@@ -356,20 +376,23 @@ def _fstar(p):
     return f
 
 
-def _epochs_to(p, f_star, runner, tol=1e-6, max_epochs=60):
-    """First 0.1-epoch checkpoint with f - f* <= tol (reading R12); runner(k) runs k updates."""
-    step = p.n // 10
-    for j in range(1, 10 * max_epochs + 1):
+def _epochs_to(p, f_star, runner, tol=1e-6, max_epochs=60, launch=0.1):
+    """First checkpoint with f - f* <= tol, f checked every `launch` epochs (0.1: reading R12;
+    1: one launch per epoch, as bench.py's value runs); runner(k) runs k updates."""
+    per = 10 if launch < 1 else 1
+    step = p.n // per
+    for j in range(1, per * max_epochs + 1):
         f = runner(step)
         if f - f_star <= tol:
-            return j / 10
+            return j / per
     return float("inf")
 
 
 @gpu
+@pytest.mark.parametrize("launch", [0.1, 1.0])
 @pytest.mark.parametrize("conc,repl,comb", [(1, 0, 0.0), (4, 0, 0.0), (16, 0, 0.0), (16, 1, 0.0), (64, 4, 0.0),
                                             (16, 0, 1e-300), (64, 0, 1e-300), (64, 0, 0.1)])
-def test_async_c1_epochs_within_1p5x_oracle(conc, repl, comb):
+def test_async_c1_epochs_within_1p5x_oracle(conc, repl, comb, launch):
     m = asaga_mod()
     p = datagen.make("c1")
     fs = _fstar(p)
@@ -381,14 +404,14 @@ def test_async_c1_epochs_within_1p5x_oracle(conc, repl, comb):
         oracle.sparse_saga(p, p.y, p.lam, g, SEED, k, st, D)
         return oracle.objective(p, p.y, p.lam, st.x)
 
-    e_or = _epochs_to(p, fs, orun)
+    e_or = _epochs_to(p, fs, orun, launch=launch)  # the oracle checked at the same cadence
     a = m.Asaga.from_problem(p, g, concurrency=conc, smem_replica_refresh=repl, combine_min_freq=comb)
 
     def grun(k):
         a.run(k, SEED)
         return a.objective()
 
-    e_gpu = _epochs_to(p, fs, grun)
+    e_gpu = _epochs_to(p, fs, grun, launch=launch)
     assert e_gpu <= 1.5 * e_or, (e_gpu, e_or)
 
 
@@ -419,6 +442,7 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl, com
     visits = a.sample_counts()
     ref = np.bincount(oracle.sample_stream(SEED, 0, T, p.n), minlength=p.n)
     assert np.array_equal(visits.astype(np.int64), ref)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, T, p.n)  # the t -> i_t map itself
     x, alpha, ab, t = a.get_state()
     assert t == T
     A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
@@ -538,7 +562,8 @@ def test_sharded_objective_single_rank_cuda():
     obj = ShardedObjective(p.n, p.d, p.lam, shard_ctx=a, device=torch.device("cuda", 0))
     x = np.random.default_rng(9).standard_normal(p.d)
     f, g = obj(torch.from_numpy(x).cuda())
-    assert f == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
+    assert f.dim() == 0 and f.is_cuda  # stays on the device (no host round trip)
+    assert float(f) == pytest.approx(oracle.objective(p, p.y, p.lam, x), rel=1e-12)
     assert rel(g.cpu().numpy(), oracle.full_grad(p, p.y, p.lam, x)) <= 1e-10
 
 
@@ -669,6 +694,7 @@ def test_bench_operating_point_c2_full_size_properties():
     assert np.log(2.0) > fs[0] > fs[2]
     ref = np.bincount(oracle.sample_stream(SEED, 0, 3 * p.n, p.n), minlength=p.n)
     assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, 3 * p.n, p.n)
     x, alpha, ab, _ = a.get_state()
     A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
     assert rel(ab, A.T @ alpha / p.n) <= 1e-10
@@ -704,6 +730,66 @@ def test_reload_async_matches_blocking_reload():
     assert got[3] == ref[3] == 5000
     st = a.stats()
     assert (st["L"], st["delta_r"], st["max_row"]) == (st_ref["L"], st_ref["delta_r"], st_ref["max_row"])
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c1", "c3s"])  # d <= 1024 (self-initialising ingest) / d > 1024
+@pytest.mark.parametrize("mode", ["blocking", "async", "host_async"])
+def test_rejected_reload_refuses_kernels_until_a_good_reload(name, mode):
+    """after a reload fails validation the context still points at the
+    rejected arrays -- every call that would launch a kernel on them returns ASAGA_E_STATE
+    (run, run_async, objective, objective_device, full_grad, partial_obj_grad), the device
+    run guard is closed, and a good reload restores the exact deterministic path."""
+    import torch
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    A = (t(p.indptr), t(p.indices), t(p.data), t(p.y))
+    g = gamma_of(p)
+    a = m.Asaga(*A, p.d, p.lam, g, deterministic=True)
+    a.run(1000, SEED)
+    bad_cols = p.indices.copy()
+    bad_cols[p.indptr[p.n // 2] + 1] = p.d + 12345  # out of range, deep inside a row
+    B = (A[0], t(bad_cols), A[2], A[3])
+    if mode == "blocking":
+        with pytest.raises(m.AsagaError) as ei:
+            a.reload(*B)
+        assert ei.value.name == "ASAGA_E_BAD_CSR"
+    else:
+        if mode == "async":
+            a.reload_async(*B)
+        else:
+            hb = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+                  for x in (p.indptr, bad_cols, p.data, p.y)]
+            a.reload_async(*hb)
+        a.run_async(p.n, SEED)  # guarded on the device: must not touch the bad columns
+        with pytest.raises(m.AsagaError) as ei:
+            a.stats()
+        assert ei.value.name == "ASAGA_E_BAD_CSR" and f"row {p.n // 2}" in str(ei.value)
+    f_dev = torch.zeros(1, dtype=torch.float64, device=dev)
+    out = torch.zeros(p.d + 1, dtype=torch.float64, device=dev)
+    x_dev = torch.zeros(p.d, dtype=torch.float64, device=dev)
+    calls = [lambda: a.run(100, SEED), lambda: a.run_async(100, SEED), lambda: a.objective(),
+             lambda: a.objective_device(f_dev), lambda: a.full_grad(),
+             lambda: a.partial_obj_grad(x_dev, out)]
+    for c in calls:
+        with pytest.raises(m.AsagaError) as ei:
+            c()
+        assert ei.value.name == "ASAGA_E_STATE", ei.value
+    torch.cuda.synchronize()
+    x, alpha, ab, _ = a.get_state()  # the state itself is readable, and finite
+    assert np.all(np.isfinite(x)) and np.all(np.isfinite(ab))
+    a.reload(*A)  # recovery: the deterministic path is exact again
+    st = oracle.State(p.n, p.d)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+    a.run(2000, SEED)
+    oracle.sparse_saga(p, p.y, p.lam, g, SEED, 2000, st, D)
+    x, alpha, ab, _ = a.get_state()
+    for got, ref in ((x, st.x), (alpha, st.alpha), (ab, st.alpha_bar)):
+        assert rel(got, ref) <= 1e-9
+    a.close()
 
 
 @gpu
@@ -1051,6 +1137,7 @@ def test_bench_operating_point_full_size_properties(name):
     f = a.objective()
     ref = np.bincount(oracle.sample_stream(SEED, 0, p.n, p.n), minlength=p.n)
     assert np.array_equal(a.sample_counts().astype(np.int64), ref)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, p.n, p.n)
     x, alpha, ab, _ = a.get_state()
     A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
     assert rel(ab, A.T @ alpha / p.n) <= 1e-10
@@ -1088,3 +1175,72 @@ def test_combine_hot_set_on_the_unfused_ingest_path():
     A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
     assert rel(ab, A.T @ alpha / p.n) <= 1e-10
     assert np.all(np.isfinite(x))
+
+
+# ---------------------------------------------------------------------- J1: async parity where value is quoted
+@gpu
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_async_budget_at_bench_operating_point(name):
+    """north_star's async criterion at the configuration bench.py's `value` is measured in:
+    full-size data, bench.OPERATING_POINT (samples in flight, gamma, layout), ONE-EPOCH
+    launches (f checked once per epoch, the regime of the timed step).  Over three sample
+    streams (the paper averages 3 runs) the mean epochs to f - f* <= 1e-6 is within
+    1.5x the oracle's epoch count at the same cadence (its 0.1-epoch count rounded up to
+    whole epochs), and so is every run's."""
+    import json
+    import math
+    import os
+
+    import bench
+
+    m = asaga_mod()
+    p = datagen.make(name)
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"fstar_{name}.json")))
+    assert gold["sha256"] == p.sha256()
+    fs = gold["f_star"]
+    budget = 1.5 * math.ceil(gold["oracle_epochs_to_1e-6"] - 1e-9)
+    op = bench.OPERATING_POINT[name]
+    a = m.Asaga.from_problem(p, op["gscale"] * gamma_of(p), concurrency=op["W"], **bench.asaga_options(op))
+    eps = []
+    for r in range(3):
+        a.set_state(np.zeros(p.d), np.zeros(p.n), np.zeros(p.d), 0)
+
+        def grun(k, r=r):
+            a.run_async(k, SEED + r)
+            return a.objective()
+
+        eps.append(_epochs_to(p, fs, grun, max_epochs=int(budget) + 2, launch=1.0))
+    a.close()
+    assert np.mean(eps) <= budget, (eps, budget)
+    assert max(eps) <= budget, (eps, budget)
+
+
+@gpu
+@pytest.mark.parametrize("name,comb", [("c1", 1e-300), ("c1", 0.1), ("c2s", 1e-300), ("c2s", 0.5)])
+def test_combine_kernel_exact_in_single_update_launches(name, comb):
+    """Exact parity of asaga_combine_kernel (the kernel the c2 bench times): a launch of ONE
+    update seeds the block replica from the shared state and flushes its pending adds at
+    exit, so a sequence of such launches is sequential Sparse SAGA (Alg. 2 with tau = 1,
+    P:259-279) computed by that kernel's own arithmetic (hot features through the replica and
+    the pending pairs, cold ones through L2).  x, alpha, abar within 1e-9 of the oracle
+    (reading R14) over 2,000 updates, with every feature hot and with a partial hot set."""
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    g = gamma_of(p)
+    a = m.Asaga.from_problem(p, g, concurrency=64, combine_min_freq=comb)
+    H = a.stats()["combine_hot"]
+    assert 0 < H <= p.d and (H == p.d) == (comb == 1e-300)
+    st = oracle.State(p.n, p.d)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+    done = 0
+    for c in (1000, 2000):
+        for _ in range(c - done):
+            a.run_async(1, SEED)
+        oracle.sparse_saga(p, p.y, p.lam, g, SEED, c - done, st, D)
+        done = c
+        x, alpha, ab, t = a.get_state()
+        assert t == done
+        for got, ref in ((x, st.x), (alpha, st.alpha), (ab, st.alpha_bar)):
+            assert rel(got, ref) <= 1e-9, (c, rel(got, ref))
+    assert a.stats()["combine_blocks"] >= 1  # launched as the combine kernel
+    a.close()

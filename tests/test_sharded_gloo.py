@@ -44,7 +44,7 @@ def _worker(rank, world, port, q):
         obj = ShardedObjective(p.n, p.d, p.lam, partial=partial)
         x = torch.from_numpy(np.random.default_rng(rank).standard_normal(p.d))  # rank 0's wins
         f, g = obj(x)
-        q.put((rank, lo, hi, f, g.numpy()))
+        q.put((rank, lo, hi, float(f), g.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -86,3 +86,45 @@ def test_shard_rows_edge_cases():
     # more ranks than rows: empty blocks allowed, still a tiling
     bl = [shard_rows(np.array([0, 1, 2]), 4, r) for r in range(4)]
     assert bl[0][0] == 0 and bl[-1][1] == 2 and all(x[0] <= x[1] for x in bl)
+
+
+def _sweep_worker(rank, world, port, q):
+    import bench
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = datagen.make("c1")
+        lam = bench.sweep_lambda(p, world, rank)
+        local_ms = 100.0 * (rank + 1)  # rank 1 is the slower one
+        value, ms = bench.job_rate(local_ms, world, p.n, 4, torch.device("cpu"))
+        q.put((rank, bench.default_workload(world), lam, value, ms))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_sweep_rank_logic_gloo():
+    """bench.py --gpus N (BASELINE config 5): each rank gets its own lambda = 10^-(r+1)/n, the
+    default workload is c3's shape, and the job's rate is all ranks' updates over the MAX of
+    the ranks' timed totals (world size 2, gloo)."""
+    import bench
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    p = datagen.make("c1")
+    assert [r[1] for r in res] == ["c3", "c3"] and bench.default_workload(1) == "c4"
+    assert res[0][2] == pytest.approx(0.1 / p.n, rel=1e-15) and res[1][2] == pytest.approx(0.01 / p.n, rel=1e-15)
+    assert bench.sweep_lambda(p, 1, 0) == p.lam
+    for _, _, _, value, ms in res:  # every rank sees the max (200 ms) and the aggregate rate
+        assert ms == 200.0
+        assert value == pytest.approx(world * p.n * 4 / 0.2, rel=1e-15)

@@ -73,7 +73,7 @@ def main():
             "unit": "evaluations/s", "n_gpus": world, "steps": args.steps, "ms_per_eval": per,
             "scaling": "strong", "config": {"workload": p.name, "n": p.n, "d": p.d, "nnz": p.nnz,
                                             "allreduce_bytes": 8 * (p.d + 1)},
-            "f": f, "grad_norm": float(torch.linalg.norm(g).item()),
+            "f": float(f), "grad_norm": float(torch.linalg.norm(g).item()),
             "rows_rank0": hi - lo}))
     shard.close()
     if world > 1:

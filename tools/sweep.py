@@ -9,6 +9,7 @@ oracle file tests/golden/fstar_<cfg>.json (written by scripts/compute_fstar.py).
     python tools/sweep.py c3 --conc 64,256,1024 --scales 1,0.5,0.25 --epochs 40
 """
 import argparse
+import itertools
 import json
 import os
 import sys
@@ -38,6 +39,9 @@ def main():
     ap.add_argument("--wt", action="store_true", help="combine_write_through")
     ap.add_argument("--maxblocks", type=int, default=0, help="combine_max_blocks")
     ap.add_argument("--persist", action="store_true", help="l2_persist_state")
+    ap.add_argument("--launch", type=float, default=0.1,
+                    help="epochs per asaga_run launch (f checked between launches): 0.1, or 1 as bench.py's value")
+    ap.add_argument("--seeds", type=int, default=1, help="sample streams per point (seed, seed+1, ...)")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -57,21 +61,25 @@ def main():
               l2_persist_state=args.persist)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
-    for W in [int(c) for c in args.conc.split(",")]:
-        for sc in [float(s) for s in args.scales.split(",")]:
+    grid = itertools.product([int(c) for c in args.conc.split(",")],
+                             [float(s) for s in args.scales.split(",")], range(args.seeds))
+    for W, sc, sd in grid:
+        if True:
             a = base
             a.reload(*A)
             a.set_concurrency(W)
             a.set_gamma(gamma0 * sc)
             stream = torch.cuda.ExternalStream(a.stream, device=dev)
-            step = p.n // 10
+            step = p.n // 10 if args.launch < 1 else p.n * int(args.launch)
+            per = step / p.n
             upd_ms = 0.0
             ep = None
             fs = []
-            for j in range(1, int(args.epochs * 10) + 1):
+            a.set_state(np.zeros(p.d), np.zeros(p.n), np.zeros(p.d), 0)
+            for j in range(1, int(args.epochs / per) + 1):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                a.run_async(step, datagen.SAMPLE_SEED)
+                a.run_async(step, datagen.SAMPLE_SEED + sd)
                 e1.record(stream)
                 f = a.objective()
                 last_ms = e0.elapsed_time(e1)
@@ -81,11 +89,11 @@ def main():
                     ep = "diverged"
                     break
                 if f - fstar <= args.tol:
-                    ep = j / 10
+                    ep = round(j * per, 6)
                     break
             st = a.stats()
             r = {"cfg": args.cfg, "W": st["concurrency"], "comb_H": st["combine_hot"], "cluster": st["combine_cluster"],
-                 "blocks": st["combine_blocks"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "epochs_to_tol": ep,
+                 "blocks": st["combine_blocks"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
                  "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
                  "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
             if st["combine_passes"]:
