@@ -144,6 +144,22 @@ typedef struct {
                             window marking the {x, abar} pair array persisting (up to the
                             device's persisting carve-out, which this raises for the process;
                             SURVEY 8(d) M6).  0 (default) = off. */
+  double pipe_late_min_freq; /* > 0: the PIPELINED update kernel (async ASAGA with the plain
+                            layout; long rows): features present in at least this fraction of
+                            rows are read as late and written as early as the sample's
+                            dependency chain allows, the other (cold) entries of the next row are
+                            gathered one sample ahead and their adds issued while the next
+                            sample's hot reads are in flight (reading R24: a bounded
+                            extra overlap on rarely shared coordinates).  Same arithmetic; with
+                            deterministic = 1 the same kernel runs sequentially.  A value above
+                            1 defers every entry.  0 (default) = the plain kernel. */
+  int pipe_merge_ns;     /* with pipe_late_min_freq > 0 (async): k > 0 = the adds to the hot
+                            features (p_v >= pipe_late_min_freq, at most 512 of them) are summed
+                            in the thread block's shared memory and sent to the shared state by
+                            its communication warp every k ns, one red.global.add.f64 per
+                            coordinate per block and flush; reads stay fresh (DESIGN.md reading
+                            R25: an add reaches the shared state up to ~k ns later).  0 (default)
+                            = every sample adds on its own.  At most 1e6. */
 } asaga_options;
 
 typedef struct {

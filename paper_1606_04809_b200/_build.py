@@ -10,7 +10,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libasaga.so")
 SOURCES = [os.path.join(CSRC, "asaga.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "asaga_kernels.cuh"), os.path.join(ROOT, "include", "asaga.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "asaga_kernels.cuh"), os.path.join(CSRC, "asaga_pipe.cuh"),
+                  os.path.join(ROOT, "include", "asaga.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

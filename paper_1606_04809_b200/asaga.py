@@ -47,7 +47,8 @@ class Options(ctypes.Structure):
                 ("measure_overlap", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double),
                 ("smem_replica_refresh", ctypes.c_int), ("combine_min_freq", ctypes.c_double),
                 ("combine_cluster", ctypes.c_int), ("combine_write_through", ctypes.c_int),
-                ("combine_max_blocks", ctypes.c_int), ("l2_persist_state", ctypes.c_int)]
+                ("combine_max_blocks", ctypes.c_int), ("l2_persist_state", ctypes.c_int),
+                ("pipe_late_min_freq", ctypes.c_double), ("pipe_merge_ns", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -178,7 +179,8 @@ class Asaga:
                  hot_split_min_freq: float = 0.0, smem_replica_refresh: int = 0,
                  combine_min_freq: float = 0.0, combine_cluster: int = 0,
                  combine_write_through: bool = False, combine_max_blocks: int = 0,
-                 l2_persist_state: bool = False):
+                 l2_persist_state: bool = False, pipe_late_min_freq: float = 0.0,
+                 pipe_merge_ns: int = 0):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -205,6 +207,8 @@ class Asaga:
         opt.combine_write_through = int(bool(combine_write_through))
         opt.combine_max_blocks = int(combine_max_blocks)
         opt.l2_persist_state = int(bool(l2_persist_state))
+        opt.pipe_late_min_freq = float(pipe_late_min_freq)
+        opt.pipe_merge_ns = int(pipe_merge_ns)
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

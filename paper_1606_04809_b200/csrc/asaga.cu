@@ -21,6 +21,7 @@
 
 #include "../../include/asaga.h"
 #include "asaga_kernels.cuh"
+#include "asaga_pipe.cuh"
 
 using namespace asaga;
 
@@ -78,6 +79,9 @@ struct asaga_ctx {
   double hot_dmax = 0.0;   // hot split threshold on D_c (abar in habar)
   int replica_every = 0;   // > 0: shared-memory replica of {x, abar} (small d, async)
   double comb_freq = 0.0;  // > 0: CTA-level combining of features with p_v >= comb_freq
+  double hot_freq = 0.0;   // > 0: the ingest computes the hot set p_v >= hot_freq (slot_of, hot_id):
+                           // comb_freq when combining, pipe_freq with pipe_merge
+  int pipe_merge = 0;      // > 0: asaga_pipe_kernel<CMB>, hot adds merged per block, flushed every this many ns
   int comb_H = 0;          // ... the number of such (hot) features after ingest
   int32_t* slot_of = nullptr;  // d: slot of a hot feature, -1 if cold
   int32_t* hot_id = nullptr;   // kCombMaxH: slot -> feature
@@ -87,6 +91,7 @@ struct asaga_ctx {
   int comb_cluster_opt = 0;    // requested cluster size (0 = 1)
   int comb_max_blocks = 0;     // cap on the combine kernel's blocks (0 = resident capacity)
   int l2_persist = 0;          // plain kernel: L2 access-policy window (persisting) over xa
+  double pipe_freq = 0.0;      // > 0: asaga_pipe_kernel, features with p_v >= it read late
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
@@ -98,6 +103,7 @@ struct asaga_ctx {
   // resolve succeeds): every entry point that launches a kernel on the matrix refuses to
   // run on rejected data (ASAGA_E_STATE) until a reload succeeds
   bool data_valid = false;
+  bool dv_ready = false;                // dv (and eslot) expanded for the current matrix
   std::string reject_msg;               // why the last ingest was rejected
   cudaEvent_t ev_part = nullptr;        // asaga_partial_obj_grad: caller stream <-> ctx stream
   bool ing_fused = false;               // the last ingest launch ran A1's finish and the report
@@ -243,8 +249,11 @@ UpdFn pick_upd_nr(int nr, bool det, int mode, bool repl) {
 int scatter_mode(const asaga_ctx* ctx);
 
 bool use_replica(const asaga_ctx* ctx);
+bool use_pipe(const asaga_ctx* ctx);
+UpdFn pipe_fn(const asaga_ctx* ctx, int lanes, int nr);
 
 UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
+  if (use_pipe(ctx)) return pipe_fn(ctx, lanes, nr);
   const bool det = ctx->deterministic != 0;
   const int mode = scatter_mode(ctx);
   const bool repl = use_replica(ctx);
@@ -256,6 +265,7 @@ UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
 }
 
 constexpr int64_t kReplicaMaxD = 4096;  // 64 KiB of {x, abar} pairs per block
+constexpr int kPipeMaxH = 512;          // pipe_merge: hot features in the per-block merge table
 constexpr int kCombMaxH = 4096;         // hot features combined per block: 128 KiB of xr + pend
 
 bool use_combine(const asaga_ctx* ctx) {
@@ -357,6 +367,49 @@ asaga_status comb_shape(asaga_ctx* ctx, int64_t workers, int* nwb, int* blocks, 
 bool use_replica(const asaga_ctx* ctx) {
   return ctx->replica_every > 0 && !ctx->deterministic && ctx->d <= kReplicaMaxD;
 }
+// the pipelined kernel: ASAGA (not the frozen-memory methods), atomic adds, no overlap counter
+bool use_pipe(const asaga_ctx* ctx) {
+  return ctx->pipe_freq > 0.0 && ctx->atomic_mode && ctx->algorithm == ASAGA_ALG_ASAGA && ctx->ov == nullptr &&
+         !use_combine(ctx);
+}
+template <int G, int NR>
+UpdFn pick_pipe(bool det, bool cmb) {
+  return det ? (cmb ? asaga_pipe_kernel<G, NR, true, true> : asaga_pipe_kernel<G, NR, true, false>)
+             : (cmb ? asaga_pipe_kernel<G, NR, false, true> : asaga_pipe_kernel<G, NR, false, false>);
+}
+template <int G>
+UpdFn pick_pipe_nr(int nr, bool det, bool cmb) {
+  switch (nr) {
+    case 1: return pick_pipe<G, 1>(det, cmb);
+    case 2: return pick_pipe<G, 2>(det, cmb);
+    case 4: return pick_pipe<G, 4>(det, cmb);
+    default: return pick_pipe<G, 8>(det, cmb);
+  }
+}
+bool use_merge(const asaga_ctx* ctx) {
+  return use_pipe(ctx) && ctx->pipe_merge > 0 && ctx->comb_H > 0 && !ctx->deterministic;
+}
+UpdFn pipe_fn(const asaga_ctx* ctx, int lanes, int nr) {
+  const bool det = ctx->deterministic != 0;
+  const bool cmb = use_merge(ctx);
+  switch (lanes) {
+    case 8: return pick_pipe_nr<8>(nr, det, cmb);
+    case 16: return pick_pipe_nr<16>(nr, det, cmb);
+    default: return pick_pipe_nr<32>(nr, det, cmb);
+  }
+}
+// pipe_merge: positions of the per-block merge table (power of two >= 2H, >= 4)
+int merge_ts(const asaga_ctx* ctx) {
+  int ts = 4;
+  while (ts < 2 * ctx->comb_H) ts *= 2;
+  return ts;
+}
+// its bytes: keys + home flags + the pending {dx, dabar} sums + the finished-groups count
+size_t merge_bytes(const asaga_ctx* ctx) {
+  if (!use_merge(ctx)) return 0;
+  const size_t ts = (size_t)merge_ts(ctx);
+  return ts * 2 * sizeof(int32_t) + ts * 2 * sizeof(double) + 16;
+}
 
 size_t replica_bytes(const asaga_ctx* ctx) {
   return use_replica(ctx) ? (((size_t)ctx->d * 16 + 15) & ~(size_t)15) : 0;
@@ -371,12 +424,28 @@ int scatter_mode(const asaga_ctx* ctx) {
 // warp, <= kBlock threads) that still gives every SM a block.  Workers packed
 // onto few SMs queue behind each other's row copies and REDs in the SM's LSU
 // (profiles/r01_update_kernel.md), so a low concurrency must not mean few SMs.
+// The smallest power-of-two block that lets one block per SM hold every worker; then one
+// block per SM (or per worker, below the SM count): the kernels deal worker groups to blocks
+// round robin, so W workers spread over min(W, #SMs) SMs (packing them into full blocks left
+// 36 of 148 SMs idle at c4's W = 448 in round 1).
 void launch_shape(const asaga_ctx* ctx, int64_t workers, int* grid, int* block) {
+  if (use_merge(ctx)) {  // gpb groups (whole warps) per block + the communication warp
+    const int64_t per_warp = 32 / ctx->lanes;
+    int64_t gpb = (workers + ctx->sms - 1) / ctx->sms;
+    gpb = (gpb + per_warp - 1) / per_warp * per_warp;
+    gpb = std::min<int64_t>(std::max<int64_t>(gpb, per_warp), ctx->max_tpb / ctx->lanes);
+    *block = (int)(gpb * ctx->lanes + 32);
+    *grid = (int)((workers + gpb - 1) / gpb);
+    return;
+  }
   const int64_t threads = workers * ctx->lanes;
   int64_t tpb = 32;
   while (tpb < ctx->max_tpb && tpb * ctx->sms < threads) tpb *= 2;
   *block = (int)tpb;
-  *grid = (int)((threads + tpb - 1) / tpb);
+  const int64_t gpb = tpb / ctx->lanes;
+  int64_t g = (workers + gpb - 1) / gpb;
+  if (g < ctx->sms) g = std::min<int64_t>(ctx->sms, workers);
+  *grid = (int)g;
 }
 
 // Pick lanes per sample and register chunks from the row-length profile, then
@@ -406,9 +475,14 @@ asaga_status configure_update(asaga_ctx* ctx) {
   // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
   // (GroupSmem in asaga_kernels.cuh)
   // (GroupSmem: bulk-scatter source buffer + 2 row stages + overflow q slots)
-  const size_t group_bytes = (size_t)nr * lanes * 2 * sizeof(double) +
-                             2 * ((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) + 16) +
-                             (size_t)ctx->overflow * sizeof(double);  // (+16: b_i per stage)
+  size_t group_bytes = (size_t)nr * lanes * 2 * sizeof(double) +
+                       2 * ((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) + 16) +
+                       (size_t)ctx->overflow * sizeof(double);  // (+16: b_i per stage)
+  if (ctx->pipe_freq > 0.0)  // the pipelined kernel's 4 stages + bounds ring (PipeSmem); the
+    // context may switch between it and the plain kernel (set_algorithm), so take the larger
+    group_bytes = std::max(group_bytes, (size_t)4 * (((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
+                                                      16 + 15) & ~(size_t)15) +
+                                            8 * 32 + (((size_t)ctx->overflow * sizeof(double) + 15) & ~(size_t)15));
   ctx->group_bytes = group_bytes;
   if (use_combine(ctx)) {
     int64_t workers = ctx->concurrency_opt > 0 ? ctx->concurrency_opt : 0;
@@ -438,11 +512,15 @@ asaga_status configure_update(asaga_ctx* ctx) {
     return ASAGA_OK;
   }
   // blocks of up to kBlock threads, fewer when long rows' overflow slots need the room
-  int tpb_max = kBlock;
-  while (tpb_max > 32 && replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes > 226 * 1024) tpb_max /= 2;
+  // (pipe_merge: up to kBlock - 32 worker threads + the communication warp)
+  const bool mg = use_merge(ctx);
+  const int comm = mg ? 32 : 0;
+  int tpb_max = kBlock - comm;
+  while (tpb_max > 32 && replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes + merge_bytes(ctx) > 226 * 1024)
+    tpb_max = mg ? tpb_max - 32 : tpb_max / 2;
   ctx->max_tpb = tpb_max;
   const int gpb = tpb_max / lanes;
-  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes;
+  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes + merge_bytes(ctx);
   UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 226 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
@@ -450,7 +528,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
   CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)ctx->smem));
   int per_sm = 0;
-  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, tpb_max, ctx->smem));
+  CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, tpb_max + comm, ctx->smem));
   per_sm = std::max(per_sm, 1);
   ctx->max_resident_groups = per_sm * ctx->sms * gpb;
   int64_t workers;
@@ -507,12 +585,12 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   CK(ctx, cudaHostAlloc(&ctx->h_ing, sizeof(unsigned long long) * (ERR_COUNT + 3), cudaHostAllocMapped));
   CK(ctx, cudaHostGetDevicePointer(&ctx->h_ing_dev, ctx->h_ing, 0));
   CK(ctx, cudaEventCreateWithFlags(&ctx->ev_ing, cudaEventDisableTiming));
-  if (ctx->comb_freq > 0.0) {
+  if (ctx->hot_freq > 0.0) {
     TRY(dalloc(ctx, &ctx->slot_of, d));
     TRY(dalloc(ctx, &ctx->hot_id, kCombMaxH));
     TRY(dalloc(ctx, &ctx->comb_flag, d));
     TRY(dalloc(ctx, &ctx->comb_excl, d));
-    TRY(dalloc(ctx, &ctx->eslot, nnz));  // written only when some features stay cold
+    if (ctx->comb_freq > 0.0) TRY(dalloc(ctx, &ctx->eslot, nnz));  // combine: written when some stay cold
     CK(ctx, cub::DeviceScan::ExclusiveSum(nullptr, ctx->cub_temp_bytes, ctx->comb_flag, ctx->comb_excl,
                                           (int)d, ctx->stream));
     unsigned char* tb = nullptr;
@@ -545,6 +623,7 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ctx->t = 0;
   ctx->snapshot_valid = false;
   ctx->data_valid = false;
+  ctx->dv_ready = false;
   if (ctx->csc_built) {  // a new matrix invalidates the column-major copy
     CK(ctx, cudaStreamSynchronize(ctx->stream));
     dfree(ctx, &ctx->csc_rows);
@@ -614,14 +693,14 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.S = ctx->S;
   ip.habar = ctx->habar;
   ip.D = ctx->D;
-  ip.comb_dmax = ctx->comb_freq > 0.0 ? 1.0 / ctx->comb_freq : 0.0;
+  ip.comb_dmax = ctx->hot_freq > 0.0 ? 1.0 / ctx->hot_freq : 0.0;
   ip.max_h = kCombMaxH;
   ip.slot_of = ctx->slot_of;
   ip.hot_id = ctx->hot_id;
   ip.flag = ctx->flag;
   ip.host_out = ctx->h_ing_dev;
   ip.row_cap = ctx->row_cap;
-  ip.hot_expected = ctx->comb_freq > 0.0 ? ctx->comb_H : -1;
+  ip.hot_expected = ctx->hot_freq > 0.0 ? ctx->comb_H : -1;
   ip.guard = guard ? 1 : 0;
   ctx->ing_fused = ip.fuse != 0;
   void* iargs[] = {&ip};
@@ -631,8 +710,8 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
                                                                           ctx->D, d, n, ctx->flag + 1);
     CK(ctx, cudaGetLastError());
   }
-  if (ctx->comb_freq > 0.0 && !ip.fuse) {  // hot set of the combine kernel: p_v >= combine_min_freq
-    hot_flag_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->D, d, 1.0 / ctx->comb_freq,
+  if (ctx->hot_freq > 0.0 && !ip.fuse) {  // hot set (combine kernel / pipe merge): p_v >= hot_freq
+    hot_flag_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->D, d, 1.0 / ctx->hot_freq,
                                                                           ctx->comb_flag);
     CK(ctx, cudaGetLastError());
     CK(ctx, cub::DeviceScan::ExclusiveSum(ctx->cub_temp, ctx->cub_temp_bytes, ctx->comb_flag, ctx->comb_excl,
@@ -649,22 +728,27 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
 asaga_status enqueue_report(asaga_ctx* ctx, bool guard) {
   if (!ctx->ing_fused) {  // (fused: written by the ingest's last block)
     ingest_report_kernel<<<1, 1, 0, ctx->stream>>>(ctx->scratch, ctx->flag, ctx->h_ing_dev, ctx->row_cap,
-                                                   ctx->comb_freq > 0.0 ? ctx->comb_H : -1, guard ? 1 : 0);
+                                                   ctx->hot_freq > 0.0 ? ctx->comb_H : -1, guard ? 1 : 0);
     CK(ctx, cudaGetLastError());
   }
   CK(ctx, cudaEventRecord(ctx->ev_ing, ctx->stream));
   return ASAGA_OK;
 }
 
-bool needs_dv(const asaga_ctx* ctx) { return !(use_combine(ctx) && ctx->comb_H == ctx->d); }
+// D per stored entry: read by the plain kernel and by the combine kernel unless every feature
+// is hot (D from its block table); the pipelined kernel gathers D_v from the d-vector itself
+bool needs_dv(const asaga_ctx* ctx) { return !(use_combine(ctx) && ctx->comb_H == ctx->d) && !use_pipe(ctx); }
 
 // D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
 // with every feature hot (which reads D from its block table) streams it with the row
+// (also lazily, from enqueue_run, when the kernel about to run needs it and the current
+// matrix has not been expanded -- e.g. after set_algorithm leaves the pipelined kernel)
 asaga_status enqueue_expand(asaga_ctx* ctx) {
   if (!needs_dv(ctx)) return ASAGA_OK;
   expand_d_kernel<<<grid_for(ctx, ctx->nnz, kBlock), kBlock, 0, ctx->stream>>>(
       ctx->cols, ctx->D, ctx->nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, ctx->d, ctx->eslot);
   CK(ctx, cudaGetLastError());
+  ctx->dv_ready = true;
   return ASAGA_OK;
 }
 
@@ -731,6 +815,12 @@ asaga_status ingest_resolve_impl(asaga_ctx* ctx) {
     if (ctx->comb_H == d && d > kCombMaxH)
       return fail(ctx, ASAGA_E_INVALID_ARG, "combine_min_freq=%g selects all %lld features; at most %d fit",
                   ctx->comb_freq, (long long)d, kCombMaxH);
+  } else if (ctx->hot_freq > 0.0) {  // pipe_merge
+    if (hflag[1] > kPipeMaxH)
+      return fail(ctx, ASAGA_E_INVALID_ARG,
+                  "pipe_late_min_freq=%g selects %d features; pipe_merge takes at most %d (raise it)",
+                  ctx->hot_freq, hflag[1], kPipeMaxH);
+    ctx->comb_H = hflag[1];
   }
   return ASAGA_OK;
 }
@@ -838,6 +928,21 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   }
   ctx->comb_max_blocks = o.combine_max_blocks;
   ctx->l2_persist = o.l2_persist_state ? 1 : 0;
+  if (!(o.pipe_late_min_freq >= 0.0) || !std::isfinite(o.pipe_late_min_freq) ||
+      (o.pipe_late_min_freq > 0.0 && (o.combine_min_freq > 0.0 || o.bulk_scatter_min_freq > 0.0 ||
+                                      o.smem_replica_refresh > 0))) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG,
+                "pipe_late_min_freq must be finite and >= 0, and cannot be combined with combining, "
+                "the bulk scatter or the replica");
+  }
+  ctx->pipe_freq = o.pipe_late_min_freq;
+  if (o.pipe_merge_ns < 0 || o.pipe_merge_ns > 1000000 || (o.pipe_merge_ns > 0 && !(o.pipe_late_min_freq > 0.0))) {
+    *ctx_out = ctx;
+    return fail(ctx, ASAGA_E_INVALID_ARG, "pipe_merge_ns must be in [0, 1e6] and needs pipe_late_min_freq > 0");
+  }
+  ctx->pipe_merge = o.pipe_merge_ns;
+  ctx->hot_freq = o.combine_min_freq > 0.0 ? o.combine_min_freq : (ctx->pipe_merge ? ctx->pipe_freq : 0.0);
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
   cudaError_t e = cudaSetDevice(o.device);
@@ -1042,7 +1147,12 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.comm_passes = ctx->comb_freq > 0.0 ? ctx->scratch + ERR_COUNT + 2 : nullptr;
   p.wt = ctx->comb_wt;
   p.split = ctx->hot_dmax > 0.0 ? 1 : 0;
+  p.late_dmax = ctx->pipe_freq > 0.0 ? 1.0 / ctx->pipe_freq : 0.0;
+  p.hot_dmax = ctx->hot_dmax;
+  p.merge_ts = use_merge(ctx) ? merge_ts(ctx) : 0;
+  p.merge_ns = ctx->pipe_merge;
   p.ok = ctx->flag + 3;  // 0 while an asynchronous reload's data does not fit this launch
+  if (needs_dv(ctx) && !ctx->dv_ready) TRY(enqueue_expand(ctx));
   if (p.comm_passes && use_combine(ctx))
     CK(ctx, cudaMemsetAsync(p.comm_passes, 0, sizeof(unsigned long long), ctx->stream));
   if (use_combine(ctx)) {
@@ -1075,7 +1185,8 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
   int grid = 1, block = 32;
   launch_shape(ctx, workers, &grid, &block);
-  const size_t smem = replica_bytes(ctx) + (size_t)(block / ctx->lanes) * ctx->group_bytes;
+  const size_t smem = replica_bytes(ctx) + (size_t)((block - (use_merge(ctx) ? 32 : 0)) / ctx->lanes) * ctx->group_bytes +
+                      merge_bytes(ctx);
   CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   if (ctx->l2_persist) {
@@ -1136,6 +1247,8 @@ void asaga_options_default(asaga_options* opt) {
   opt->combine_write_through = 0;
   opt->combine_max_blocks = 0;
   opt->l2_persist_state = 0;
+  opt->pipe_late_min_freq = 0.0;
+  opt->pipe_merge_ns = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

@@ -800,6 +800,10 @@ struct UpdateParams {
   unsigned long long* comm_passes;  // += communication-warp passes (asaga_stats)
   int wt;                 // combine_write_through: hot adds go straight to L2 (replica reads only)
   int split;              // hot split in use (entries with dv < 0 keep abar in habar)
+  double late_dmax;       // asaga_pipe_kernel: entries with |D_c| <= late_dmax are hot (read late)
+  double hot_dmax;        // asaga_pipe_kernel: hot split of features with D_c <= hot_dmax
+  int merge_ts;           // asaga_pipe_kernel<CMB>: merge-table positions (power of 2 >= 2H)
+  int merge_ns;           // ... flush period of the communication warp (ns)
   const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
 };
 
@@ -901,7 +905,9 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   const int g = lane & (G - 1);
   const unsigned gmask =
       (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (unsigned)(lane & ~(G - 1)));
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  // groups are dealt to blocks round robin (w = group slot * grid + block): with at least
+  // as many workers as SMs every SM runs some (launch_shape puts one block on each)
+  const int64_t w = (int64_t)(threadIdx.x / G) * gridDim.x + blockIdx.x;
   double2* rx = reinterpret_cast<double2*>(smem_raw);  // REPL replica (first in smem)
   const size_t repl_bytes = REPL ? (((size_t)p.repl_d * sizeof(double2) + 15) & ~(size_t)15) : 0;
   if (REPL) {  // fill before any early exit: the whole block takes part in the barrier
@@ -981,7 +987,12 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         if (REPL)
           xb[j] = rx[c];
         else if (p.split && sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
+#ifdef ASAGA_TIMING
+          xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x),
+                               (p.debug_mode & 8) ? 0.0 : ld_na(p.habar + c));  // bit3: no hot abar ops
+#else
           xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c));
+#endif
         else
           xb[j] = ld_na2(p.xa + (int64_t)c * p.S);
       }
@@ -1063,8 +1074,16 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
           dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : db * a * p.inv_n);
         } else if (MODE >= 1) {
+#ifdef ASAGA_TIMING
+          // bit4: no x RED for hot (split) entries; bit5: no REDs at all for cold entries
+          const bool hot_e = abv != xv + 1;
+          if (!((p.debug_mode & 16) && hot_e) && !((p.debug_mode & 32) && !hot_e)) red_add(xv, ngam * u);
+          if (!p.frozen && !((p.debug_mode & 8) && hot_e) && !((p.debug_mode & 32) && !hot_e))
+            red_add(abv, db * a * p.inv_n);
+#else
           red_add(xv, ngam * u);
           if (!p.frozen) red_add(abv, db * a * p.inv_n);
+#endif
         } else {
           st_cg(xv, ld_cg(xv) + ngam * u);
           if (!p.frozen) st_cg(abv, ld_cg(abv) + db * a * p.inv_n);

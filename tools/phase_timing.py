@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--bulk", type=float, default=0.0, help="bulk_scatter_min_freq")
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
     ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
+    ap.add_argument("--pipe", type=float, default=0.0, help="pipe_late_min_freq")
+    ap.add_argument("--merge", type=int, default=0, help="pipe_merge_ns")
     args = ap.parse_args()
     import importlib.util
 
@@ -45,11 +47,15 @@ def main():
               atomic=bool(args.atomic), lanes_per_sample=args.lanes,
               bulk_scatter_min_freq=args.bulk,
               hot_split_min_freq=args.split,
-              smem_replica_refresh=args.repl)
+              smem_replica_refresh=args.repl, pipe_late_min_freq=args.pipe,
+              pipe_merge_ns=args.merge)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     buf = (ctypes.c_ulonglong * 9)()
     names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail", "-", "s_wait_read", "s_compute",
              "s_fence"]
+    if args.pipe > 0:  # asaga_pipe_kernel's phases (asaga_pipe.cuh)
+        names = ["hot_gather_issue", "cold_scatter_prev", "wait_copy", "dot_wait", "reduce_sigma", "-",
+                 "hot_scatter", "merge_dstore_cold_gather", "wait_dload"]
     for W in [int(c) for c in args.conc.split(",")]:
         a.set_concurrency(W)
         a.run(p.n, 1)
@@ -59,9 +65,12 @@ def main():
         it = max(buf[5], 1)
         st = a.stats()
         cyc = [buf[k] / it for k in range(9)]
-        # phases 6-8 split the scatter phase [3] (their sum is <= it: marks inside it)
-        print(f"{args.cfg} G={st['lanes_per_sample']} bulk={args.bulk} split={args.split} repl={args.repl} W={st['concurrency']} "
-              f"upd/s={p.n / st['last_run_ms'] * 1e3:.4g} cycles/sample total={sum(cyc[:5]):.0f}: "
+        # plain kernel: phases 6-8 split the scatter phase [3] (their sum is <= it: marks inside
+        # it); pipelined kernel: every phase but [5] (the iteration count) is disjoint
+        total = sum(c for k, c in enumerate(cyc) if k != 5) if args.pipe > 0 else sum(cyc[:5])
+        print(f"{args.cfg} G={st['lanes_per_sample']} bulk={args.bulk} split={args.split} repl={args.repl} "
+              f"pipe={args.pipe} W={st['concurrency']} "
+              f"upd/s={p.n / st['last_run_ms'] * 1e3:.4g} cycles/sample total={total:.0f}: "
               + " ".join(f"{n}={c:.0f}" for n, c in zip(names, cyc) if n != "-"))
 
 

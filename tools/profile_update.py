@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--split", type=float, default=0.0, help="hot_split_min_freq")
     ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     ap.add_argument("--comb", type=float, default=0.0, help="combine_min_freq")
+    ap.add_argument("--pipe", type=float, default=0.0, help="pipe_late_min_freq")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -32,7 +33,8 @@ def main():
     a = Asaga(t(p.indptr), t(p.indices), t(p.data), t(p.y), p.d, p.lam, 1.0, concurrency=args.conc,
               bulk_scatter_min_freq=args.bulk,
               hot_split_min_freq=args.split,
-              smem_replica_refresh=args.repl, combine_min_freq=args.comb)
+              smem_replica_refresh=args.repl, combine_min_freq=args.comb,
+              pipe_late_min_freq=args.pipe)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     T = args.updates or p.n
     a.run(T, datagen.SAMPLE_SEED)  # warm-up launch
