@@ -607,6 +607,16 @@ def main():
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),
         }
+        ceil = (load_json("profiles", "r02_ceilings.json") or {}).get(p.name)
+        if ceil and op["comb"] == 0:
+            # the kernel against the saturated rate of its own access pattern at any number in
+            # flight (both measured in the same, timing, build: profiles/r02_update_kernel.md)
+            out["roofline_in_situ"] = {
+                "bound": "L2 service of the kernel's own access pattern (popular x lines + cold traffic)",
+                "achieved_timing_build": ceil["full_at_W_bench"], "peak_timing_build": ceil["full_max_any_W"],
+                "frac": ceil["full_at_W_bench"] / ceil["full_max_any_W"],
+                "hot_ops_only_timing_build": ceil["hot_only_max"], "unit": "updates/s",
+                "source": "profiles/r02_ceilings.json (timing build, same W and layout as this line)"}
         tr = load_json("profiles", "traffic.json") or {}
         if p.name in tr:
             # ncu cannot run inside the timed bench: the DRAM bytes of one launch of the same

@@ -17,6 +17,7 @@ Functions and the passages they follow:
   objective / full_grad         Section 4.1
   sparse_saga                   Eq. 3 + Section 4.2, Alg. 2 order
   delayed_saga                  Assumption 1 at its bound; NEXT-1 tool
+  replica_saga                  Section 5 periodic exchange between replicas; NEXT-3 tool
   hogwild / svrg_*              Section 4.3 comparison methods, SPEC S:230-237,
                                 S:306-307, regulariser projected as in Section 4.2 (R21)
 All are pinned in tests/test_oracle_pins.py; none is "parity unpinned".
@@ -77,6 +78,8 @@ def _load():
                                           u64, u64, u64, _F64P, _F64P, _F64P]),
             "oracle_delayed_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                            u64, u64, u64, i64, _F64P, _F64P, _F64P]),
+            "oracle_replica_saga": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
+                                           u64, u64, u64, i64, i64, _F64P, _F64P, _F64P]),
             "oracle_hogwild": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, f64, f64,
                                       u64, u64, u64, _F64P]),
             "oracle_svrg_snapshot": (None, [i64, i64, _I64P, _I32P, _F64P, _F64P, _F64P, _F64P,
@@ -234,6 +237,25 @@ def delayed_saga(A, y, lam, gamma, seed, T: int, tau: int, state: State | None =
         D = reweight(n, column_counts(A))
     _load().oracle_delayed_saga(n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P),
                                 _p(y, _F64P), _p(D, _F64P), lam, gamma, seed, state.t, T, tau,
+                                _p(state.x, _F64P), _p(state.alpha, _F64P),
+                                _p(state.alpha_bar, _F64P))
+    state.t += T
+    return state
+
+
+def replica_saga(A, y, lam, gamma, seed, T: int, N: int, E: int, state: State | None = None, D=None):
+    """NEXT-3 model (Section 5): N replicas of (x, abar), update t on replica t mod N,
+    each replica's own updates applied to its copy at once, every copy reset to the shared
+    value plus everyone's changes every E updates (and at the end)."""
+    n, d, indptr, indices, data = _csr(A)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    if state is None:
+        state = State(n, d)
+    if D is None:
+        D = reweight(n, column_counts(A))
+    assert N >= 1 and E >= 1
+    _load().oracle_replica_saga(n, d, _p(indptr, _I64P), _p(indices, _I32P), _p(data, _F64P),
+                                _p(y, _F64P), _p(D, _F64P), lam, gamma, seed, state.t, T, N, E,
                                 _p(state.x, _F64P), _p(state.alpha, _F64P),
                                 _p(state.alpha_bar, _F64P))
     state.t += T

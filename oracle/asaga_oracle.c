@@ -264,6 +264,79 @@ void oracle_delayed_saga(int64_t n, int64_t d, const int64_t* indptr,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Replicated Sparse SAGA with periodic exchange (NEXT-3 tool; Section 5, P:569:
+ * "limiting communications can be interpreted as artificially increasing the delay").
+ * N replicas (GPUs) each hold a copy of (x, abar); the global update counter t is dealt
+ * round robin, update t runs on replica r = (t - t0) mod N.  An update reads replica r's
+ * copy and alpha_i, computes Alg. 2's step exactly as oracle_saga_step (pre-step values,
+ * reading R8) and applies it to replica r's copy at once; every E global updates (and
+ * after the last) the replicas exchange: the shared (x, abar) receives the sum of every
+ * replica's changes since the previous exchange and every copy becomes the shared value.
+ * A replica's copy is kept as the shared value plus its own pending changes (x_r =
+ * x + dx_r), with the pending coordinates listed, so an exchange costs the coordinates
+ * touched.  alpha is one shared array (a sample's memory; reading R26: a repeat of i on
+ * two replicas inside one exchange window, probability ~E/n, reads the current alpha_i).
+ * N = 1, or E = 1, is sequential Sparse SAGA up to the rounding of x + dx (pinned).   */
+void oracle_replica_saga(int64_t n, int64_t d, const int64_t* indptr,
+                         const int32_t* indices, const double* data, const double* y,
+                         const double* D, double lambda, double gamma, uint64_t seed,
+                         uint64_t t0, uint64_t T, int64_t N, int64_t E, double* x,
+                         double* alpha, double* alpha_bar) {
+  const double inv_n = 1.0 / (double)n;
+  int64_t maxrow = 1;
+  for (int64_t i = 0; i < n; ++i)
+    if (indptr[i + 1] - indptr[i] > maxrow) maxrow = indptr[i + 1] - indptr[i];
+  double* u = (double*)malloc(sizeof(double) * (size_t)maxrow);
+  double* dx = (double*)calloc((size_t)(N * d), sizeof(double));
+  double* dab = (double*)calloc((size_t)(N * d), sizeof(double));
+  unsigned char* mark = (unsigned char*)calloc((size_t)(N * d), 1);
+  int32_t* list = (int32_t*)malloc(sizeof(int32_t) * (size_t)(N * d));
+  int64_t* cnt = (int64_t*)calloc((size_t)N, sizeof(int64_t));
+  for (uint64_t step = 0; step < T; ++step) {
+    const int64_t r = (int64_t)(step % (uint64_t)N);
+    double* dxr = dx + r * d;
+    double* dabr = dab + r * d;
+    int64_t i = (int64_t)oracle_sample_index(seed, t0 + step, (uint64_t)n);
+    int64_t lo = indptr[i], hi = indptr[i + 1];
+    double z = 0.0;
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      z += data[k] * (x[v] + dxr[v]);
+    }
+    double s = oracle_sigma(y[i], z);
+    double dalpha = s - alpha[i];
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      u[k - lo] = dalpha * data[k] + D[v] * ((alpha_bar[v] + dabr[v]) + lambda * (x[v] + dxr[v]));
+    }
+    for (int64_t k = lo; k < hi; ++k) {
+      int32_t v = indices[k];
+      dxr[v] = dxr[v] - gamma * u[k - lo];
+      dabr[v] = dabr[v] + dalpha * data[k] * inv_n;
+      if (!mark[r * d + v]) {
+        mark[r * d + v] = 1;
+        list[r * d + cnt[r]++] = v;
+      }
+    }
+    alpha[i] = alpha[i] + dalpha;
+    if ((step + 1) % (uint64_t)E == 0 || step + 1 == T) {  /* exchange, replicas in order */
+      for (int64_t q = 0; q < N; ++q) {
+        for (int64_t j = 0; j < cnt[q]; ++j) {
+          int32_t v = list[q * d + j];
+          x[v] = x[v] + dx[q * d + v];
+          alpha_bar[v] = alpha_bar[v] + dab[q * d + v];
+          dx[q * d + v] = 0.0;
+          dab[q * d + v] = 0.0;
+          mark[q * d + v] = 0;
+        }
+        cnt[q] = 0;
+      }
+    }
+  }
+  free(u); free(dx); free(dab); free(mark); free(list); free(cnt);
+}
+
+/* ------------------------------------------------------------------------ */
 /* Comparison methods of Section 4.3, NEXT-2.  Both follow SPEC's
  * serial forms with the D_i-projected regulariser of
  * Section 4.2 applied uniformly (reading R21).

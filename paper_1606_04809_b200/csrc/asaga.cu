@@ -404,11 +404,12 @@ int merge_ts(const asaga_ctx* ctx) {
   while (ts < 2 * ctx->comb_H) ts *= 2;
   return ts;
 }
-// its bytes: keys + home flags + the pending {dx, dabar} sums + the finished-groups count
-size_t merge_bytes(const asaga_ctx* ctx) {
+// its bytes for gpb worker groups: keys + home flags + per group a row of running sums and
+// a row of sent sums (2 x {dx, dabar}) + the finished-groups count
+size_t merge_bytes(const asaga_ctx* ctx, int gpb) {
   if (!use_merge(ctx)) return 0;
   const size_t ts = (size_t)merge_ts(ctx);
-  return ts * 2 * sizeof(int32_t) + ts * 2 * sizeof(double) + 16;
+  return ts * 2 * sizeof(int32_t) + (size_t)gpb * 2 * ts * 2 * sizeof(double) + 16;
 }
 
 size_t replica_bytes(const asaga_ctx* ctx) {
@@ -516,11 +517,12 @@ asaga_status configure_update(asaga_ctx* ctx) {
   const bool mg = use_merge(ctx);
   const int comm = mg ? 32 : 0;
   int tpb_max = kBlock - comm;
-  while (tpb_max > 32 && replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes + merge_bytes(ctx) > 226 * 1024)
+  while (tpb_max > 32 &&
+         replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes + merge_bytes(ctx, tpb_max / lanes) > 226 * 1024)
     tpb_max = mg ? tpb_max - 32 : tpb_max / 2;
   ctx->max_tpb = tpb_max;
   const int gpb = tpb_max / lanes;
-  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes + merge_bytes(ctx);
+  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes + merge_bytes(ctx, gpb);
   UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 226 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
@@ -1185,8 +1187,8 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   int64_t workers = std::min<int64_t>(ctx->workers, (int64_t)std::min<uint64_t>(n_updates, (uint64_t)INT64_MAX));
   int grid = 1, block = 32;
   launch_shape(ctx, workers, &grid, &block);
-  const size_t smem = replica_bytes(ctx) + (size_t)((block - (use_merge(ctx) ? 32 : 0)) / ctx->lanes) * ctx->group_bytes +
-                      merge_bytes(ctx);
+  const int groups = (block - (use_merge(ctx) ? 32 : 0)) / ctx->lanes;
+  const size_t smem = replica_bytes(ctx) + (size_t)groups * ctx->group_bytes + merge_bytes(ctx, groups);
   CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   if (ctx->l2_persist) {

@@ -37,10 +37,14 @@
 // kernel's own expressions, for exact parity against the oracle.
 //
 // CMB = true (option pipe_merge_ns, async only): at step 6 a worker adds its HOT entries'
-// {dx, dabar} into the block's pending table in shared memory (feature -> position by a
-// shared-memory hash of the hot set; f64 shared atomics), and the block's communication
-// warp sends each position's accumulated sum to L2 with one red.global.add.f64 per
-// coordinate every merge_ns nanoseconds (exchange with 0, then RED).  Reads stay fresh
+// {dx, dabar} into ITS OWN row of the block's table in shared memory (feature -> position
+// by a shared-memory hash of the hot set; plain loads and stores, no atomics: a row has
+// one writer and only grows), and every merge_ns nanoseconds the block's communication
+// warp sends, per position, the growth of every worker row since its previous look (row
+// value minus the value it last sent, kept in its own array) to L2 with one
+// red.global.add.f64 per coordinate.  (Shared f64 atomicAdd is a CAS loop on sm_100a:
+// the first version, one shared pending sum per position, spent ~3k cycles per sample in
+// those loops.)  Reads stay fresh
 // loads from L2 (steps 1 and 7): only the hot ADDS wait, by at most one flush period plus
 // the pass, in the block before they reach the shared state -- an iteration counted "in
 // progress to the end of the writing of its update" (Assumption 1), so the
@@ -96,8 +100,9 @@ __device__ __forceinline__ void pipe_row_copy(unsigned char* gbase, int stage, c
 }
 
 // CMB: the per-block merge table after the worker groups' blocks (asaga.cu sizes it):
-// keys[TS] (feature, -1 empty), home[TS] (1: abar in habar), pend[TS] {dx, dabar}, and the
-// count of finished worker groups; the block's last warp is the communication warp
+// keys[TS] (feature, -1 empty), home[TS] (1: abar in habar), acc[groups][TS] {dx, dabar}
+// (each worker's running sums), sent[groups][TS] (what the communication warp has sent of
+// them), and the count of finished worker groups; the block's last warp communicates
 __device__ __forceinline__ unsigned hot_hash(int v) { return (unsigned)v * 2654435761u; }
 
 template <int G, int NR, bool DET, bool CMB>
@@ -123,13 +128,17 @@ __global__ void __launch_bounds__(256, 1) asaga_pipe_kernel(UpdateParams p) {
   const int TS = CMB ? p.merge_ts : 0;
   int32_t* mkey = reinterpret_cast<int32_t*>(smem_raw + (size_t)ngrp * SM::bytes(p.overflow));
   int32_t* mhome = mkey + TS;
-  double2* pend = reinterpret_cast<double2*>(mhome + TS);  // 16-B aligned (TS >= 4)
-  int* mdone = reinterpret_cast<int*>(pend + TS);
+  double2* macc = reinterpret_cast<double2*>(mhome + TS);  // [ngrp][TS], 16-B aligned (TS >= 4)
+  double2* msent = macc + (size_t)ngrp * TS;                // [ngrp][TS]
+  int* mdone = reinterpret_cast<int*>(msent + (size_t)ngrp * TS);
   if (CMB) {
     for (int k = threadIdx.x; k < TS; k += blockDim.x) {
       mkey[k] = -1;
       mhome[k] = 0;
-      pend[k] = make_double2(0.0, 0.0);
+    }
+    for (int k = threadIdx.x; k < ngrp * TS; k += blockDim.x) {
+      macc[k] = make_double2(0.0, 0.0);
+      msent[k] = make_double2(0.0, 0.0);
     }
     if (threadIdx.x == 0) *mdone = 0;
     __syncthreads();
@@ -147,10 +156,15 @@ __global__ void __launch_bounds__(256, 1) asaga_pipe_kernel(UpdateParams p) {
         for (int k = lane_c; k < TS; k += 32) {
           const int v = mkey[k];
           if (v < 0) continue;
-          const double dx = __longlong_as_double((long long)atomicExch(
-              reinterpret_cast<unsigned long long*>(&pend[k].x), 0ull));
-          const double dy = __longlong_as_double((long long)atomicExch(
-              reinterpret_cast<unsigned long long*>(&pend[k].y), 0ull));
+          double dx = 0.0, dy = 0.0;
+          for (int q = 0; q < ngrp; ++q) {  // the growth of every worker's running sum
+            const volatile double* a = reinterpret_cast<const volatile double*>(macc + (size_t)q * TS + k);
+            const double ax = a[0], ay = a[1];
+            double2* sp = msent + (size_t)q * TS + k;
+            dx += ax - sp->x;
+            dy += ay - sp->y;
+            *sp = make_double2(ax, ay);
+          }
           double* xv = &p.xa[(int64_t)v * p.S].x;
           if (dx != 0.0) red_add(xv, dx);
           if (dy != 0.0) red_add(mhome[k] ? p.habar + v : xv + 1, dy);
@@ -392,10 +406,11 @@ __global__ void __launch_bounds__(256, 1) asaga_pipe_kernel(UpdateParams p) {
         if (DET || fabs(dvv) <= late) {
           const int c = scol(sb, e);
           const int pos = (CMB && fabs(dvv) <= late) ? mpos(c) : -1;
-          if (pos >= 0) {  // the block's pending sum (flushed by the communication warp)
+          if (pos >= 0) {  // this worker's running sum (sent by the communication warp)
             const double a = sval(sb, e);
-            atomicAdd(&pend[pos].x, ngam * fma(db, a, qq[j]));
-            atomicAdd(&pend[pos].y, db * a * p.inv_n);
+            volatile double* acc = reinterpret_cast<volatile double*>(macc + (size_t)grp * TS + pos);
+            acc[0] = acc[0] + ngam * fma(db, a, qq[j]);
+            acc[1] = acc[1] + db * a * p.inv_n;
           } else {
             scatter(c, dvv, sval(sb, e), qq[j], db);
           }
@@ -471,7 +486,8 @@ __global__ void __launch_bounds__(256, 1) asaga_pipe_kernel(UpdateParams p) {
   cp_async_wait_all();
   if (p.visits && g == 0) atomicAdd(p.shash, shash);
   if (CMB) {
-    __syncwarp(gmask);  // every lane's pending adds are in
+    __threadfence_block();  // this lane's running sums are visible to the communication warp
+    __syncwarp(gmask);
     if (g == 0) atomicAdd(mdone, 1);
   }
 #ifdef ASAGA_TIMING

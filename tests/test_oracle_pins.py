@@ -428,6 +428,72 @@ def test_delayed_tau1_by_hand():
     assert np.allclose(got.alpha, st.alpha, rtol=1e-14, atol=1e-15)
 
 
+# --------------------------------------------------------------------------- NEXT-3 replicated model
+def test_replica_reduces_to_sequential():
+    """One replica (any exchange period) or an exchange after every update is sequential
+    Sparse SAGA: E = 1 bit for bit (x + 0 is exact), N = 1 up to the rounding of x + dx."""
+    p = datagen.make("c1")
+    g = 1 / (3 * oracle.lipschitz(p, p.lam))
+    a = oracle.sparse_saga(p, p.y, p.lam, g, SEED, 5000)
+    for N in (2, 5):
+        b = oracle.replica_saga(p, p.y, p.lam, g, SEED, 5000, N, 1)
+        assert np.array_equal(a.x, b.x) and np.array_equal(a.alpha, b.alpha)
+        assert np.array_equal(a.alpha_bar, b.alpha_bar)
+    for E in (7, 1000, 10**9):
+        c = oracle.replica_saga(p, p.y, p.lam, g, SEED, 5000, 1, E)
+        for u, v in ((c.x, a.x), (c.alpha, a.alpha), (c.alpha_bar, a.alpha_bar)):
+            assert np.linalg.norm(u - v) <= 1e-13 * np.linalg.norm(v)
+
+
+def test_replica_schedule_by_hand_and_quiescent_identity():
+    """N = 3 replicas exchanging every E = 4 updates on a tiny problem, against the schedule
+    written out with explicit copies (each replica steps its own copy with the shared alpha;
+    at an exchange the shared state gains every copy's change); then the quiescent identity
+    abar = (1/n) sum alpha_i a_i holds after the final exchange."""
+    p = datagen.random_tiny(5, 6, 8, density=0.5)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+    g, N, E, T = 0.4, 3, 4, 23
+    got = oracle.replica_saga(p, p.y, p.lam, g, SEED, T, N, E, D=D)
+    idx = oracle.sample_stream(SEED, 0, T, p.n)
+    shared = fresh(p)
+    copies = [shared.copy() for _ in range(N)]
+    for t in range(T):
+        r = t % N
+        c = copies[r]
+        c.alpha = shared.alpha  # one shared memory of alpha (reading R26)
+        oracle.saga_step(p, p.y, p.lam, g, int(idx[t]), c, D)
+        if (t + 1) % E == 0 or t + 1 == T:
+            base_x, base_ab = shared.x.copy(), shared.alpha_bar.copy()
+            for q in range(N):
+                shared.x = shared.x + (copies[q].x - base_x)
+                shared.alpha_bar = shared.alpha_bar + (copies[q].alpha_bar - base_ab)
+            for q in range(N):
+                copies[q].x, copies[q].alpha_bar = shared.x.copy(), shared.alpha_bar.copy()
+    assert np.allclose(got.x, shared.x, rtol=1e-12, atol=1e-15)
+    assert np.allclose(got.alpha, shared.alpha, rtol=1e-12, atol=1e-15)
+    assert np.allclose(got.alpha_bar, shared.alpha_bar, rtol=1e-12, atol=1e-15)
+    q = datagen.make("c1")
+    gq = 1 / (3 * oracle.lipschitz(q, q.lam))
+    st = oracle.replica_saga(q, q.y, q.lam, gq, SEED, 7 * q.n + 3, 4, 64)
+    assert np.allclose(st.alpha_bar, csr(q).T @ st.alpha / q.n, rtol=0, atol=1e-12)
+
+
+def test_replica_fixed_point_is_stationary():
+    """P9 for the replicated model: at (x*, alpha_i = sigma_i(x*), abar = mean) every
+    replica's every update is zero, whatever the exchange period."""
+    p = datagen.make("c1")
+    g = 1 / (3 * oracle.lipschitz(p, p.lam))
+    x = newton_opt(p)
+    A = csr(p)
+    alpha = -p.y / (1.0 + np.exp(p.y * (A @ x)))
+    st = fresh(p)
+    st.x = x.copy()
+    st.alpha = alpha
+    st.alpha_bar = A.T @ alpha / p.n
+    oracle.replica_saga(p, p.y, p.lam, g, SEED, 10 * p.n, 8, 256, st)
+    assert np.abs(st.x - x).max() <= 1e-10
+
+
 # --------------------------------------------------------------------------- NEXT-2 comparison methods
 def test_svrg_first_inner_step_reference_identity():
     """At x = x~ the data difference vanishes: the step is -gamma (D mu + lambda D x) on S_i."""
