@@ -31,6 +31,7 @@ constexpr int kBlock = 256;
 constexpr int kColSeg = 2048;         // CSC entries per gradient segment
 constexpr int64_t kSmemHistMax = 48 * 1024;  // columns held in a shared histogram
 constexpr int64_t kSelfInitMaxD = 1024;      // the ingest initialises itself (no init launch)
+constexpr int kIngestHashLogRows = 14;        // rows-mode ingest: 16K-slot hash cache (128 KiB)
 
 thread_local std::string g_thread_err = "no error";
 
@@ -657,8 +658,12 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.nnz = nnz;
   ip.smem_hist = d <= kSmemHistMax ? 1 : 0;
   const double mean_row = n > 0 ? (double)nnz / (double)n : 0.0;
+  // the hash cache of n_v for large d: long rows (one row per warp step) take a larger one
+  // (more of the Zipf-popular columns counted in shared memory instead of global atomics)
+  ip.hash_log = (!ip.smem_hist && mean_row >= 32.0) ? kIngestHashLogRows : kHashLog;
   const size_t hist_bytes =
-      ((ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * (size_t)kHashSlots * sizeof(int32_t)) + 15) & ~(size_t)15;
+      ((ip.smem_hist ? (size_t)d * sizeof(int32_t) : 2 * ((size_t)1 << ip.hash_log) * sizeof(int32_t)) + 15) &
+      ~(size_t)15;
   // short rows: warp stages (kStageCap entries per warp) when they fit next to the histogram
   const size_t stage_bytes = 32 * (size_t)kStageCap * (sizeof(double) + sizeof(int32_t));
   const bool staged = n > 0 && mean_row <= 16.0 && hist_bytes + stage_bytes <= 200 * 1024;

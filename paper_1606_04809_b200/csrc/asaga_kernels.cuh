@@ -224,7 +224,8 @@ struct IngestParams {
   int hot_expected;
   int guard;
   int smem_hist;          // 1: per-block shared histogram of all d columns; 0: a per-block
-                          // shared hash cache of kHashSlots columns (the popular ones claim it)
+                          // shared hash cache of 2^hash_log columns (the popular ones claim it)
+  int hash_log;           // !smem_hist: log2 of the hash cache's slots (kHashLog, or larger)
   // self_init (fused, d <= kSelfInitMaxD): no ingest_init launch -- every block stores its
   // histogram into part[block][d] (no atomics, no zeroed counts), zeroes alpha for its rows,
   // and the last block sums the parts into counts, then (after the report) resets the error
@@ -302,7 +303,8 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
   __shared__ long long blk_len[32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   int32_t* hkey = hist;                  // !smem_hist: hash cache keys (-1 = free) ...
-  int32_t* hcnt = hist + kHashSlots;     // ... and counts
+  const int hslots = 1 << p.hash_log;
+  int32_t* hcnt = hist + hslots;         // ... and counts
   // STAGED: per-warp stages after the histogram (p.stage_off bytes into dynamic smem)
   double* stage_v = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(hist) + p.stage_off) +
                     (size_t)wib * kStageCap;
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     } else {
       // n_v: a Zipf-popular column would take ~1e6 serialised global atomics (c4: 4.8 ms
       // of the ingest); the first column to hash into a free slot keeps it per block
-      const int slot = (int)(((unsigned)c * 2654435761u) >> (32 - kHashLog));
+      const int slot = (int)(((unsigned)c * 2654435761u) >> (32 - p.hash_log));
       int k = hkey[slot];
       if (k == -1) {
         const int prev = atomicCAS(&hkey[slot], -1, c);
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
   if (p.smem_hist) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x) hist[v] = 0;
   } else {
-    for (int k = threadIdx.x; k < kHashSlots; k += blockDim.x) {
+    for (int k = threadIdx.x; k < hslots; k += blockDim.x) {
       hkey[k] = -1;
       hcnt[k] = 0;
     }
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
     for (int64_t v = threadIdx.x; v < p.d; v += blockDim.x)
       if (hist[v]) atomicAdd(&p.counts[v], hist[v]);
   } else {
-    for (int k = threadIdx.x; k < kHashSlots; k += blockDim.x)
+    for (int k = threadIdx.x; k < hslots; k += blockDim.x)
       if (hkey[k] >= 0 && hcnt[k]) atomicAdd(&p.counts[hkey[k]], hcnt[k]);
   }
   if (p.fuse) {  // the last block to finish runs A1's finish and the report (d <= 4096)
