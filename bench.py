@@ -625,7 +625,7 @@ def main():
             out["roofline"]["traffic_source"] = ("stored: dram__bytes_read.sum + dram__bytes_write.sum of one "
                                                  "update launch (one epoch) from an ncu --set full capture "
                                                  "(profiles/traffic.json), not measured in this run")
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # (the contract: rank 0 at N = 1 only)
             out["cpu_baseline"] = cpu_baseline(p, lam, 1.0 / (3.0 * L), args.cpu_seconds)
         print(json.dumps(out))
     a.close()
