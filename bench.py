@@ -95,9 +95,11 @@ OPERATING_POINT = {
     "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
     # c2: every feature combined per thread block (asaga_combine_kernel), 46 workers per SM
     "c2": dict(W=6808, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
-    # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split)
-    "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.3, repl=0, comb=0.0),
-    "c4": dict(W=448, gscale=0.25, bulk=0.0, split=0.3, repl=0, comb=0.0),
+    # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split);
+    # rows staged by 1-D TMA bulk copies on c3 (+4.5 % update rate), by per-element cp.async
+    # on c4 (2.5 % faster there; profiles/r02_update_kernel.md)
+    "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.3, repl=0, comb=0.0, rowcp=0),
+    "c4": dict(W=448, gscale=0.25, bulk=0.0, split=0.3, repl=0, comb=0.0, rowcp=1),
 }
 
 
@@ -105,7 +107,8 @@ def asaga_options(op):
     """Asaga keyword options of an operating point."""
     return dict(bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
                 smem_replica_refresh=op["repl"], combine_min_freq=op["comb"],
-                l2_persist_state=bool(op.get("persist", False)))
+                l2_persist_state=bool(op.get("persist", False)),
+                row_copy_elementwise=bool(op.get("rowcp", 0)))
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:

@@ -160,6 +160,11 @@ typedef struct {
                             coordinate per block and flush; reads stay fresh (DESIGN.md reading
                             R25: an add reaches the shared state up to ~k ns later).  0 (default)
                             = every sample adds on its own.  At most 1e6. */
+  int row_copy_elementwise; /* plain update kernel's row staging: 0 (default) = 1-D TMA bulk
+                            copies (cp.async.bulk, completing on an mbarrier; three per row,
+                            issued by one lane) when the column / value / D arrays are 16-B
+                            aligned, else per-element cp.async; 1 = always per-element cp.async.
+                            Same data, same arithmetic. */
 } asaga_options;
 
 typedef struct {

@@ -48,7 +48,8 @@ class Options(ctypes.Structure):
                 ("smem_replica_refresh", ctypes.c_int), ("combine_min_freq", ctypes.c_double),
                 ("combine_cluster", ctypes.c_int), ("combine_write_through", ctypes.c_int),
                 ("combine_max_blocks", ctypes.c_int), ("l2_persist_state", ctypes.c_int),
-                ("pipe_late_min_freq", ctypes.c_double), ("pipe_merge_ns", ctypes.c_int)]
+                ("pipe_late_min_freq", ctypes.c_double), ("pipe_merge_ns", ctypes.c_int),
+                ("row_copy_elementwise", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -180,7 +181,7 @@ class Asaga:
                  combine_min_freq: float = 0.0, combine_cluster: int = 0,
                  combine_write_through: bool = False, combine_max_blocks: int = 0,
                  l2_persist_state: bool = False, pipe_late_min_freq: float = 0.0,
-                 pipe_merge_ns: int = 0):
+                 pipe_merge_ns: int = 0, row_copy_elementwise: bool = False):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -209,6 +210,7 @@ class Asaga:
         opt.l2_persist_state = int(bool(l2_persist_state))
         opt.pipe_late_min_freq = float(pipe_late_min_freq)
         opt.pipe_merge_ns = int(pipe_merge_ns)
+        opt.row_copy_elementwise = int(bool(row_copy_elementwise))
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

@@ -93,6 +93,7 @@ struct asaga_ctx {
   int comb_max_blocks = 0;     // cap on the combine kernel's blocks (0 = resident capacity)
   int l2_persist = 0;          // plain kernel: L2 access-policy window (persisting) over xa
   double pipe_freq = 0.0;      // > 0: asaga_pipe_kernel, features with p_v >= it read late
+  int row_copy_elementwise = 0;  // plain kernel: per-element cp.async row staging (no TMA bulk)
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
@@ -477,9 +478,13 @@ asaga_status configure_update(asaga_ctx* ctx) {
   // per group: 2 stages of nr*lanes row entries (int32 + fp64) + overflow q slots
   // (GroupSmem in asaga_kernels.cuh)
   // (GroupSmem: bulk-scatter source buffer + 2 row stages + overflow q slots)
-  size_t group_bytes = (size_t)nr * lanes * 2 * sizeof(double) +
-                       2 * ((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) + 16) +
-                       (size_t)ctx->overflow * sizeof(double);  // (+16: b_i per stage)
+  // GroupSmem in asaga_kernels.cuh: the bulk-scatter source buffer + 2 stages (values and
+  // D with 2 slots of 16-B alignment slack, columns with 4, b_i + the stage's mbarrier) +
+  // the overflow q slots
+  const size_t P = (size_t)nr * lanes;
+  size_t group_bytes = P * 2 * sizeof(double) +
+                       2 * (2 * (P + 2) * sizeof(double) + (P + 4) * sizeof(int32_t) + 16) +
+                       (size_t)ctx->overflow * sizeof(double);
   if (ctx->pipe_freq > 0.0)  // the pipelined kernel's 4 stages + bounds ring (PipeSmem); the
     // context may switch between it and the plain kernel (set_algorithm), so take the larger
     group_bytes = std::max(group_bytes, (size_t)4 * (((size_t)nr * lanes * (sizeof(int32_t) + 2 * sizeof(double)) +
@@ -949,6 +954,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
     return fail(ctx, ASAGA_E_INVALID_ARG, "pipe_merge_ns must be in [0, 1e6] and needs pipe_late_min_freq > 0");
   }
   ctx->pipe_merge = o.pipe_merge_ns;
+  ctx->row_copy_elementwise = o.row_copy_elementwise ? 1 : 0;
   ctx->hot_freq = o.combine_min_freq > 0.0 ? o.combine_min_freq : (ctx->pipe_merge ? ctx->pipe_freq : 0.0);
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
@@ -1158,6 +1164,11 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.hot_dmax = ctx->hot_dmax;
   p.merge_ts = use_merge(ctx) ? merge_ts(ctx) : 0;
   p.merge_ns = ctx->pipe_merge;
+  // 1-D TMA row staging when the arrays the kernel streams are 16-B aligned (the caller's
+  // borrowed arrays may be offset views)
+  p.nnz = ctx->nnz;
+  p.bulk_rows = ((((uintptr_t)ctx->cols) | ((uintptr_t)ctx->vals) | ((uintptr_t)ctx->dv)) & 15) == 0 &&
+                !ctx->row_copy_elementwise;
   p.ok = ctx->flag + 3;  // 0 while an asynchronous reload's data does not fit this launch
   if (needs_dv(ctx) && !ctx->dv_ready) TRY(enqueue_expand(ctx));
   if (p.comm_passes && use_combine(ctx))
@@ -1256,6 +1267,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->l2_persist_state = 0;
   opt->pipe_late_min_freq = 0.0;
   opt->pipe_merge_ns = 0;
+  opt->row_copy_elementwise = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

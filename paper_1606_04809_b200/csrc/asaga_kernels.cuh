@@ -614,6 +614,9 @@ __global__ void expand_d_kernel(const int32_t* __restrict__ cols, const double* 
     for (int u = 0; u < U; ++u) {
       const int64_t k = k0 + (int64_t)u * blockDim.x;
       c[u] = k < nnz ? __ldcs(cols + k) : 0;
+      // an asynchronous reload expands before its validation is read back: an index out of
+      // [0, d) must not be dereferenced (the data is rejected; dv is never used then)
+      if ((unsigned long long)(unsigned)c[u] >= (unsigned long long)d) c[u] = 0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) Dc[u] = __ldg(D + c[u]);
@@ -822,23 +825,63 @@ struct UpdateParams {
   double hot_dmax;        // asaga_pipe_kernel: hot split of features with D_c <= hot_dmax
   int merge_ts;           // asaga_pipe_kernel<CMB>: merge-table positions (power of 2 >= 2H)
   int merge_ns;           // ... flush period of the communication warp (ns)
+  int bulk_rows;          // asaga_update_kernel: stage rows by 1-D TMA bulk copies (cols, vals, dv
+                          // 16-B aligned); 0 = per-element cp.async
+  int64_t nnz;            // stored entries (bulk copies never read past them)
   const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
 };
 
 // Shared memory per group: a P-entry {dx, dabar} source buffer for the TMA bulk
-// scatter (16-B aligned, first), 2 stages x P = NR*G row entries (fp64 value,
-// fp64 D, int32 index), then `overflow` fp64 q slots for rows longer than P.
+// scatter (16-B aligned, first), 2 stages of the first P = NR*G row entries, then
+// `overflow` fp64 q slots for rows longer than P.  A stage holds the row's values, D's and
+// columns from 16-B aligned starts (a bulk copy moves whole 16-B units: up to 1 leading
+// fp64 / 3 leading int32 of the previous row come along, so entry e of the row sits at
+// slot (lo & 1) + e / (lo & 3) + e), then b_i and the stage's mbarrier.
 template <int G, int NR>
 struct GroupSmem {
   static constexpr int P = NR * G;
+  static constexpr int PV = P + 2;  // fp64 slots: 1 leading + 1 trailing of alignment slack
+  static constexpr int PC = P + 4;  // int32 slots: 3 leading + 1 trailing
   static constexpr size_t delta_bytes = (size_t)P * 2 * sizeof(double);
-  // a stage: P values, P D's, P columns, then b_i (16-B slot; P * 20 is a multiple of 16)
-  static constexpr size_t stage_bytes = (size_t)P * (2 * sizeof(double) + sizeof(int32_t)) + 16;
-  static constexpr size_t label_off = (size_t)P * (2 * sizeof(double) + sizeof(int32_t));
+  static constexpr size_t vals_off = 0;
+  static constexpr size_t dv_off = (size_t)PV * sizeof(double);
+  static constexpr size_t cols_off = 2 * (size_t)PV * sizeof(double);
+  static constexpr size_t label_off = cols_off + (size_t)PC * sizeof(int32_t);  // 16-B multiple
+  static constexpr size_t mbar_off = label_off + 8;
+  static constexpr size_t stage_bytes = label_off + 16;
   static __host__ __device__ size_t bytes(int overflow) {
     return delta_bytes + 2 * stage_bytes + (size_t)overflow * sizeof(double);
   }
 };
+
+// 1-D TMA (cp.async.bulk) helpers: a global -> shared copy completing on an mbarrier
+// (transaction bytes), issued by one lane; the group waits on the barrier's phase.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(void* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(void* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(void* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(void* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, void* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
 
 // TMA bulk reduction of one {x, abar} pair: a single 16-byte .add.f64 performed at
 // L2 by the async proxy (UBLKRED) -- one L2 operation instead of two REDs on the
@@ -856,28 +899,51 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Row staging of the plain update kernel: the first P entries of the row (values, D per
+// entry, columns) into a stage.  bulk: lane 0 issues three 1-D TMA copies of the 16-B
+// aligned supersets (UBLKCP: three instructions per row instead of 3 ceil(len/G) LDGSTS per
+// lane), completing on the stage's mbarrier; otherwise (misaligned caller arrays, or the
+// last rows, whose aligned superset would read past nnz) per-element cp.async, and lane 0
+// arrives on the barrier without transaction bytes.  b_i always by cp.async.
 template <int G, int NR>
 __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, const int32_t* cols,
                                                const double* vals, const double* dv, const double* b_i,
-                                               int64_t lo, int64_t hi, int g) {
+                                               int64_t lo, int64_t hi, int g, int bulk, int64_t nnz) {
+  using GS = GroupSmem<G, NR>;
   constexpr int P = NR * G;
-  double* sv = reinterpret_cast<double*>(base + GroupSmem<G, NR>::delta_bytes +
-                                         stage * GroupSmem<G, NR>::stage_bytes);
-  if (g == 0)
-    cp_async8(reinterpret_cast<unsigned char*>(sv) + GroupSmem<G, NR>::label_off, b_i);
-  double* sd = sv + P;
-  int32_t* sc = reinterpret_cast<int32_t*>(sd + P);
-  const int len = (int)(hi - lo);
+  unsigned char* sb = base + GS::delta_bytes + stage * GS::stage_bytes;
+  double* sv = reinterpret_cast<double*>(sb + GS::vals_off);
+  double* sd = reinterpret_cast<double*>(sb + GS::dv_off);
+  int32_t* sc = reinterpret_cast<int32_t*>(sb + GS::cols_off);
+  void* bar = sb + GS::mbar_off;
+  if (g == 0) cp_async8(sb + GS::label_off, b_i);
   const uint64_t pol = policy_evict_first();
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    if (j * G >= len) break;  // group-uniform: no predicated-off chunks
-    const int64_t k = lo + j * G + g;
-    if (j * G + g < len) {
-      cp_async4_ef(sc + j * G + g, cols + k, pol);
-      cp_async8_ef(sv + j * G + g, vals + k, pol);
-      cp_async8_ef(sd + j * G + g, dv + k, pol);
+  const int64_t hs = hi - lo > P ? lo + P : hi;  // staged entries [lo, hs)
+  const int64_t lo_c = lo & ~(int64_t)3, hi_c = (hs + 3) & ~(int64_t)3;
+  const int64_t lo_v = lo & ~(int64_t)1, hi_v = (hs + 1) & ~(int64_t)1;
+  if (bulk && hi_c <= nnz && hi_v <= nnz) {  // group-uniform
+    if (g == 0) {
+      const unsigned bc = (unsigned)((hi_c - lo_c) * 4), bv = (unsigned)((hi_v - lo_v) * 8);
+      fence_proxy_async_smem();  // earlier generic reads of this stage before the async writes
+      mbar_arrive_tx(bar, bc + 2 * bv);
+      bulk_g2s(sc, cols + lo_c, bc, bar, pol);
+      bulk_g2s(sv, vals + lo_v, bv, bar, pol);
+      bulk_g2s(sd, dv + lo_v, bv, bar, pol);
     }
+  } else {
+    const int len = (int)(hs - lo);
+    const int oc = (int)(lo & 3), ov = (int)(lo & 1);
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      if (j * G >= len) break;  // group-uniform: no predicated-off chunks
+      const int64_t k = lo + j * G + g;
+      if (j * G + g < len) {
+        cp_async4_ef(sc + oc + j * G + g, cols + k, pol);
+        cp_async8_ef(sv + ov + j * G + g, vals + k, pol);
+        cp_async8_ef(sd + ov + j * G + g, dv + k, pol);
+      }
+    }
+    if (g == 0) mbar_arrive(bar);  // (the data is waited for with cp.async.wait_all)
   }
   cp_async_commit();
 }
@@ -946,6 +1012,15 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   if (t >= tend) return;
   const uint64_t W = (uint64_t)p.workers;
   const uint64_t t_first = t;
+  // the two stages' mbarriers (one arrival per use: lane 0's expect_tx or plain arrive)
+  using GS = GroupSmem<G, NR>;
+  if (g == 0) {
+    mbar_init(gbase + GS::delta_bytes + GS::mbar_off, 1);
+    mbar_init(gbase + GS::delta_bytes + GS::stage_bytes + GS::mbar_off, 1);
+    mbar_init_fence();
+  }
+  __syncwarp(gmask);
+  unsigned phase_bits = 0;  // bit s: parity of stage s's next completion
   // sample indices in batches of G: lane j draws sample mb + j of this worker (one Philox
   // per lane per G samples), shuffled out in order (group-uniform calls)
   int64_t bi = 0;
@@ -963,7 +1038,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   int64_t i = sample_of(0);
   int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
   int stage = 0;
-  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, p.y + i, lo, hi, g);
+  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, p.y + i, lo, hi, g, p.bulk_rows, p.nnz);
   int64_t in1 = 0, lo1 = 0, hi1 = 0, in2 = 0;
   in1 = sample_of(1);
   in2 = sample_of(2);
@@ -984,15 +1059,16 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     // ---- pass 1: row entries (shared memory), gathers, dot product
     const int len = (int)(hi - lo);
     cp_async_wait_all();
+    unsigned char* sbase = gbase + GS::delta_bytes + stage * GS::stage_bytes;
+    mbar_wait(sbase + GS::mbar_off, (phase_bits >> stage) & 1u);
+    phase_bits ^= 1u << stage;
     TMARK(0);
-    const double* sv = reinterpret_cast<const double*>(gbase + GroupSmem<G, NR>::delta_bytes +
-                                                       stage * GroupSmem<G, NR>::stage_bytes);
-    const double* sd = sv + P;
-    const int32_t* sc = reinterpret_cast<const int32_t*>(sd + P);
+    const double* sv = reinterpret_cast<const double*>(sbase + GS::vals_off) + (lo & 1);
+    const double* sd = reinterpret_cast<const double*>(sbase + GS::dv_off) + (lo & 1);
+    const int32_t* sc = reinterpret_cast<const int32_t*>(sbase + GS::cols_off) + (lo & 3);
     // b_i came with the row (carrying it in registers next to the row bounds measured 9 %
     // slower on c3; a plain load next to alpha_i's, 2 %)
-    const double yb = *reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(sv) +
-                                                       GroupSmem<G, NR>::label_off);
+    const double yb = *reinterpret_cast<const double*>(sbase + GS::label_off);
     // gathers of x^, abar^ and D for every resident chunk are issued before any use
     double qq[NR];
     double2 xb[NR];
@@ -1038,7 +1114,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
 #else
     constexpr bool copy_late = false;
 #endif
-    if (has1 && !copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g);
+    if (has1 && !copy_late)
+      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
     int64_t lo2 = 0, hi2 = 0;
     if (has2) {
       lo2 = __ldg(&p.rowptr[in2]);
@@ -1065,7 +1142,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       dot = fma(a, v.x, dot);
       qs[k - lo - P] = fabs(Dv) * fma(p.lambda_, v.x, v.y);
     }
-    if (has1 && copy_late) issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g);
+    if (has1 && copy_late)
+      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
     TMARK(1);
     // ---- scalar derivative (folded logistic) and memory difference
     dot = group_sum<G>(dot, gmask) * yb;  // folded margin b_i a_i . x^ (exact: b = +-1)

@@ -128,11 +128,12 @@ def test_sigma_device_function_accuracy():
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
-def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0):
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False):
     m = asaga_mod()
     g = gamma_of(prob)
     a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
-                             bulk_scatter_min_freq=bulk, hot_split_min_freq=split)
+                             bulk_scatter_min_freq=bulk, hot_split_min_freq=split,
+                             row_copy_elementwise=elementwise)
     st = oracle.State(prob.n, prob.d)
     D = oracle.reweight(prob.n, oracle.column_counts(prob))
     done = 0
@@ -184,10 +185,42 @@ def test_deterministic_hot_split(name, split):
 
 @gpu
 @pytest.mark.parametrize("name", ["c2s", "c3s", "c4s"])
-def test_deterministic_subsets(name):
-    """Config recipes at oracle size: several tiles, ragged rows, long-row overflow path."""
+@pytest.mark.parametrize("elementwise", [False, True])
+def test_deterministic_subsets(name, elementwise):
+    """Config recipes at oracle size: several tiles, ragged rows, long-row overflow path; rows
+    staged by 1-D TMA bulk copies (the last rows, whose aligned superset would pass nnz, by the
+    per-element fallback) and by per-element cp.async throughout."""
     p = SUBSETS[name]()
-    _det_compare(p, 60_000, [1, 10_000, 60_000])
+    _det_compare(p, 60_000, [1, 10_000, 60_000], elementwise=elementwise)
+
+
+@gpu
+def test_bulk_row_staging_with_misaligned_borrowed_arrays():
+    """Borrowed device arrays that are offset views (column and value arrays not 16-B
+    aligned: the 1-D TMA copy cannot take them) fall back to per-element staging and give
+    the same deterministic iterate as aligned ones, bit for bit, and the oracle's (1e-9)."""
+    import torch
+
+    m = asaga_mod()
+    p = SUBSETS["c3s"]()
+    g = gamma_of(p)
+    dev = torch.device("cuda", 0)
+    ci = torch.zeros(len(p.indices) + 1, dtype=torch.int32, device=dev)
+    cv = torch.zeros(len(p.data) + 1, dtype=torch.float64, device=dev)
+    ci[1:] = torch.from_numpy(p.indices).to(dev)
+    cv[1:] = torch.from_numpy(p.data).to(dev)
+    ip, yy = torch.from_numpy(p.indptr).to(dev), torch.from_numpy(p.y).to(dev)
+    mis = m.Asaga(ip, ci[1:], cv[1:], yy, p.d, p.lam, g, deterministic=True)
+    ali = m.Asaga(ip, torch.from_numpy(p.indices).to(dev), torch.from_numpy(p.data).to(dev), yy, p.d,
+                  p.lam, g, deterministic=True)
+    assert ci[1:].data_ptr() % 16 != 0 and cv[1:].data_ptr() % 16 != 0
+    mis.run(20_000, SEED)
+    ali.run(20_000, SEED)
+    xm, am, bm, _ = mis.get_state()
+    xa, aa, ba, _ = ali.get_state()
+    assert np.array_equal(xm, xa) and np.array_equal(am, aa) and np.array_equal(bm, ba)
+    st = oracle.sparse_saga(p, p.y, p.lam, g, SEED, 20_000)
+    assert rel(xm, st.x) <= 1e-9 and rel(am, st.alpha) <= 1e-9
 
 
 @gpu
