@@ -10,6 +10,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -214,6 +216,21 @@ void dfree(asaga_ctx* ctx, T** p) {
     if (s_ != ASAGA_OK) return s_;   \
   } while (0)
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize, raised only when a launch needs more than was
+// set before (per device and function, process-wide): the attribute call cost host time on
+// every launch of the 0.1-epoch convergence loops
+cudaError_t ensure_smem_attr(int device, const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_pair(device, fn);
+  const auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[key] = bytes;
+  return e;
+}
+
 int grid_for(const asaga_ctx* ctx, int64_t work, int block) {
   int64_t g = (work + block - 1) / block;
   int64_t cap = (int64_t)ctx->sms * 8;
@@ -337,7 +354,7 @@ asaga_status comb_shape(asaga_ctx* ctx, int64_t workers, int* nwb, int* blocks, 
     cfg.dynamicSmemBytes = 200 * 1024;  // forces one block per SM
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(ctx, ensure_smem_attr(ctx->device, (const void*)fn, 200 * 1024));
     CK(ctx, cudaOccupancyMaxActiveClusters(&cap_clusters, (const void*)fn, &cfg));
   }
   if (cap_clusters < 1) return fail(ctx, ASAGA_E_INVALID_ARG, "no cluster of %d blocks fits the device", C);
@@ -506,8 +523,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
                   "combine: %d hot features and %d workers per block need %zu B of shared memory "
                   "(raise combine_min_freq or lower the concurrency)", ctx->comb_H, nwb, ctx->smem);
     UpdFn cfn = combine_fn(ctx, lanes, nr);
-    CK(ctx, cudaFuncSetAttribute((const void*)cfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)ctx->smem));
+    CK(ctx, ensure_smem_attr(ctx->device, (const void*)cfn, (int)ctx->smem));
     ctx->comb_nwb = nwb;
     ctx->comb_csize = csize;
     ctx->workers = workers;
@@ -533,8 +549,7 @@ asaga_status configure_update(asaga_ctx* ctx) {
   if (ctx->smem > 226 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
                 (long long)ctx->max_row);
-  CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)ctx->smem));
+  CK(ctx, ensure_smem_attr(ctx->device, (const void*)fn, (int)ctx->smem));
   int per_sm = 0;
   CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, tpb_max + comm, ctx->smem));
   per_sm = std::max(per_sm, 1);
@@ -685,7 +700,7 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   const int kIngestBlock = 1024;
   const int rows_per_warp = 32;
   // (the attribute is per function, shared by every context: set it on every launch)
-  CK(ctx, cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
+  CK(ctx, ensure_smem_attr(ctx->device, kfn, (int)hsmem));
   if (ctx->ingest_grid == 0) {  // once per context (n, d fixed)
     int per_sm = 1;
     CK(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kIngestBlock, hsmem));
@@ -1190,7 +1205,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
     cfg.stream = ctx->stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CK(ctx, cudaFuncSetAttribute((const void*)cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    CK(ctx, ensure_smem_attr(ctx->device, (const void*)cfn, (int)ctx->smem));
     if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
     CK(ctx, cudaLaunchKernelEx(&cfg, cfn, p));
     if (timed) CK(ctx, cudaEventRecord(ctx->ev1, ctx->stream));
@@ -1205,7 +1220,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   launch_shape(ctx, workers, &grid, &block);
   const int groups = (block - (use_merge(ctx) ? 32 : 0)) / ctx->lanes;
   const size_t smem = replica_bytes(ctx) + (size_t)groups * ctx->group_bytes + merge_bytes(ctx, groups);
-  CK(ctx, cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(ctx, ensure_smem_attr(ctx->device, (const void*)fn, (int)smem));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   if (ctx->l2_persist) {
     // the {x, abar} pairs as a persisting L2 window for this launch only
