@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--persist", action="store_true", help="l2_persist_state")
     ap.add_argument("--pipe", type=float, default=0.0, help="pipe_late_min_freq (pipelined kernel)")
     ap.add_argument("--merge", type=int, default=0, help="pipe_merge_ns")
+    ap.add_argument("--rowcp", action="store_true", help="row_copy_elementwise")
     ap.add_argument("--launch", type=float, default=0.1,
                     help="epochs per asaga_run launch (f checked between launches): 0.1, or 1 as bench.py's value")
     ap.add_argument("--seeds", type=int, default=1, help="sample streams per point (seed, seed+1, ...)")
@@ -61,7 +62,7 @@ def main():
               combine_cluster=args.cluster, lanes_per_sample=args.lanes,
               combine_write_through=args.wt, combine_max_blocks=args.maxblocks,
               l2_persist_state=args.persist, pipe_late_min_freq=args.pipe,
-              pipe_merge_ns=args.merge)
+              pipe_merge_ns=args.merge, row_copy_elementwise=args.rowcp)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     grid = itertools.product([int(c) for c in args.conc.split(",")],
