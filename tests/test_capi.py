@@ -65,6 +65,9 @@ def test_update_kernel_sass_uses_l2_atomics_and_l1_bypass(libpath):
     assert "LDG.E.NA.128" in sass  # one L1-bypassing 16-byte {x, abar} gather per entry
     assert "LDGSTS" in sass  # cp.async copy of the next sample's row into shared memory
     assert "HMMA" not in sass and "UTCHMMA" not in sass  # no tensor-core path here
+    # round 2: rows staged by 1-D TMA bulk copies completing on an mbarrier
+    assert "UBLKCP" in sass  # cp.async.bulk global -> shared (the plain kernel's row stages)
+    assert "SYNCS" in sass  # mbarrier arrive.expect_tx / try_wait
 
 
 def test_product_never_imports_oracle():
