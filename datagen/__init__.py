@@ -114,51 +114,80 @@ def _zipf_cdf(d: int, s: float) -> np.ndarray:
     return c / c[-1]
 
 
+def _distinct_prefix_block(u, need, m, d, cdf):
+    """One block of rows: u = their stream values (rows back to back, m[r] each), need = the
+    distinct values wanted per row.  Returns (ok per row, ranks, rank_in_row, keep) for the
+    block -- rows are independent, so blocks of rows may be processed separately (and
+    concurrently) with the result of processing them all at once."""
+    rows = np.repeat(np.arange(len(need), dtype=np.int64), m)
+    ranks = np.searchsorted(cdf, u, side="right").astype(np.int64)
+    np.minimum(ranks, d - 1, out=ranks)
+    key = rows * d + ranks
+    order = np.argsort(key, kind="stable")  # stable: stream order inside equal keys
+    ks = key[order]
+    first_sorted = np.ones(len(ks), dtype=bool)
+    first_sorted[1:] = ks[1:] != ks[:-1]
+    first = np.zeros(len(ks), dtype=bool)
+    first[order] = first_sorted  # first occurrence, back in stream order
+    # running count of distinct values per row, in stream order
+    cnt = np.cumsum(first)
+    row_start = np.concatenate([[0], np.cumsum(m)[:-1]])
+    base = np.concatenate([[0], cnt])[row_start]
+    rank_in_row = cnt - np.repeat(base, m)
+    keep = first & (rank_in_row <= np.repeat(need, m))
+    got = np.bincount(rows[keep], minlength=len(need))
+    return got == need, rows, ranks, rank_in_row, keep
+
+
 def _first_distinct_rows(rng, lens: np.ndarray, d: int, cdf: np.ndarray, perm: np.ndarray):
     """Per row i: the first lens[i] distinct values of an i.i.d. stream drawn from cdf.
 
     Each round draws a batch of 2*lens+8 stream values per unfinished row and keeps
     the first lens[i] distinct ones in stream order; a row whose batch holds fewer
     distinct values is redrawn from a fresh, twice longer stream.  Either way the
-    row is the first-lens[i]-distinct prefix of an i.i.d. Zipf stream."""
+    row is the first-lens[i]-distinct prefix of an i.i.d. Zipf stream.  (A round's values
+    are drawn block of rows by block of rows -- the same stream as one draw -- and the
+    blocks are processed on a thread pool: the output does not depend on the blocking.)"""
+    from concurrent.futures import ThreadPoolExecutor
+
     n = len(lens)
     indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(lens, out=indptr[1:])
     out = np.empty(int(indptr[-1]), dtype=np.int64)
     todo = np.arange(n, dtype=np.int64)
     factor = 2
-    while len(todo):
-        need = lens[todo]
-        m = factor * need + 8
-        rows = np.repeat(np.arange(len(todo), dtype=np.int64), m)
-        ranks = np.searchsorted(cdf, rng.random(int(m.sum())), side="right").astype(np.int64)
-        np.minimum(ranks, d - 1, out=ranks)
-        key = rows * d + ranks
-        order = np.argsort(key, kind="stable")  # stable: stream order inside equal keys
-        ks = key[order]
-        first_sorted = np.ones(len(ks), dtype=bool)
-        first_sorted[1:] = ks[1:] != ks[:-1]
-        first = np.zeros(len(ks), dtype=bool)
-        first[order] = first_sorted  # first occurrence, back in stream order
-        # running count of distinct values per row, in stream order
-        cnt = np.cumsum(first)
-        row_start = np.concatenate([[0], np.cumsum(m)[:-1]])
-        base = np.concatenate([[0], cnt])[row_start]
-        rank_in_row = cnt - np.repeat(base, m)
-        keep = first & (rank_in_row <= np.repeat(need, m))
-        got = np.bincount(rows[keep], minlength=len(todo))
-        ok = got == need
-        # rows with enough distinct values: write them (sorted later)
-        sel = keep & np.repeat(ok, m)
-        dst_rows = todo[rows[sel]]
-        # position within row = rank_in_row - 1
-        out[indptr[dst_rows] + rank_in_row[sel] - 1] = ranks[sel]
-        todo = todo[~ok]
-        factor *= 2
-    cols = perm[out]
-    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
-    cols = np.sort(rows * d + cols) - rows * d  # strictly increasing inside each row
-    return indptr, cols.astype(np.int32)
+    block = 65536
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
+        while len(todo):
+            need_all = lens[todo]
+            m_all = factor * need_all + 8
+            futs = []
+            for b0 in range(0, len(todo), block):
+                need, m = need_all[b0:b0 + block], m_all[b0:b0 + block]
+                u = rng.random(int(m.sum()))  # consecutive draws: the same stream as one draw
+                futs.append((b0, pool.submit(_distinct_prefix_block, u, need, m, d, cdf)))
+            ok_all = np.zeros(len(todo), dtype=bool)
+            for b0, f in futs:
+                ok, rows, ranks, rank_in_row, keep = f.result()
+                ok_all[b0:b0 + len(ok)] = ok
+                m = m_all[b0:b0 + len(ok)]
+                sel = keep & np.repeat(ok, m)
+                dst_rows = todo[b0 + rows[sel]]
+                out[indptr[dst_rows] + rank_in_row[sel] - 1] = ranks[sel]  # position = rank - 1
+            todo = todo[~ok_all]
+            factor *= 2
+
+        cols = perm[out]
+
+        def sort_rows(r0, r1):  # strictly increasing inside each row (rows are independent)
+            a, b = int(indptr[r0]), int(indptr[r1])
+            rr = np.repeat(np.arange(r0, r1, dtype=np.int64), lens[r0:r1])
+            return a, (np.sort(rr * d + cols[a:b]) - rr * d).astype(np.int32)
+
+        res = np.empty(int(indptr[-1]), dtype=np.int32)
+        for a, v in pool.map(lambda r: sort_rows(r, min(n, r + block)), range(0, n, block)):
+            res[a:a + len(v)] = v
+    return indptr, res
 
 
 def _gen_c1(n, d, k):
