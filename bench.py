@@ -93,8 +93,10 @@ class pinned_core:
 # the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
 OPERATING_POINT = {
     "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
-    # c2: every feature combined per thread block (asaga_combine_kernel), 46 workers per SM
-    "c2": dict(W=6808, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
+    # c2: every feature combined per thread block (asaga_combine_kernel), 40 workers per SM
+    # (W = 6808, 46 per SM, is 7 % faster but sits at the edge: one round-end test run saw
+    # all three streams miss 1e-6 in 15 one-epoch launches; 5920 gives 11 epochs with margin)
+    "c2": dict(W=5920, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
     # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split);
     # rows staged by 1-D TMA bulk copies on c3 (+4.5 % update rate), by per-element cp.async
     # on c4 (2.5 % faster there; profiles/r02_update_kernel.md)

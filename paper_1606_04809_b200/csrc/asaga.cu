@@ -1753,6 +1753,10 @@ void asaga_destroy(asaga_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->l2_persist) {  // give the persisting L2 carve-out this context raised back to the device
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+  }
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev_ing) cudaEventDestroy(ctx->ev_ing);
