@@ -634,15 +634,19 @@ def main():
                 "samples_in_flight": st["concurrency"],
                 "source": "tools/microbench (profiles/microbench_b200.json), clock64 phases (profiles/r01_update_kernel.md)"}
         ceil = (load_json("profiles", "r02_ceilings.json") or {}).get(p.name)
-        if ceil and op["comb"] == 0:
-            # the kernel against the saturated rate of its own access pattern at any number in
-            # flight (both measured in the same, timing, build: profiles/r02_update_kernel.md)
+        if maxtp is not None and op["comb"] == 0:
+            # the update kernel against the saturated rate of its own access pattern: the best
+            # rate over the samples in flight scanned in THIS run (max_throughput_point); the
+            # profiling build's hot-operations-only rate is the context (r02_update_kernel.md)
+            peak_sat = max(r["updates_per_s"] for r in maxtp["scan"])
             out["roofline_in_situ"] = {
-                "bound": "L2 service of the kernel's own access pattern (popular x lines + cold traffic)",
-                "achieved_timing_build": ceil["full_at_W_bench"], "peak_timing_build": ceil["full_max_any_W"],
-                "frac": ceil["full_at_W_bench"] / ceil["full_max_any_W"],
-                "hot_ops_only_timing_build": ceil["hot_only_max"], "unit": "updates/s",
-                "source": "profiles/r02_ceilings.json (timing build, same W and layout as this line)"}
+                "bound": "L2 service of the kernel's own access pattern (popular x lines + cold traffic): "
+                         "the best rate at any number in flight, this run",
+                "achieved": ups, "peak": peak_sat, "unit": "updates/s", "frac": ups / peak_sat,
+                "peak_at_samples_in_flight": max(maxtp["scan"], key=lambda r: r["updates_per_s"])["samples_in_flight"],
+                "hot_ops_only_vs_full_timing_build": (ceil or {}).get("hot_only_max", 0) / ceil["full_max_any_W"]
+                if ceil else None,
+                "source": "max_throughput_point.scan (this run); profiles/r02_ceilings.json (profiling build)"}
         tr = load_json("profiles", "traffic.json") or {}
         if p.name in tr:
             # ncu cannot run inside the timed bench: the DRAM bytes of one launch of the same
