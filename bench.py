@@ -92,7 +92,9 @@ class pinned_core:
 # feature frequency) from tools/sweep.py on B200 (profiles/r01_operating_point.md):
 # the fastest time-to-1e-6 whose epoch count stays within 1.5x the oracle's.
 OPERATING_POINT = {
-    "c1": dict(W=16, gscale=1.0, bulk=0.0, split=0.0, repl=0, comb=0.0),
+    # c1 (n = 1000): 64 in flight = 6.4 % of n (Thm 2 asks tau < n/10) at half the step:
+    # 11-13 epochs in one-epoch launches (W = 16, gamma 1/(3L): 12-14 at a third of the rate)
+    "c1": dict(W=64, gscale=0.5, bulk=0.0, split=0.0, repl=0, comb=0.0),
     # c2: every feature combined per thread block (asaga_combine_kernel), 40 workers per SM
     # (W = 6808, 46 per SM, is 7 % faster but sits at the edge: one round-end test run saw
     # all three streams miss 1e-6 in 15 one-epoch launches; 5920 gives 11 epochs with margin)
