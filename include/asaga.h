@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define ASAGA_ABI_VERSION 2
+#define ASAGA_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define ASAGA_API __attribute__((visibility("default")))
@@ -165,6 +165,15 @@ typedef struct {
                             issued by one lane) when the column / value / D arrays are 16-B
                             aligned, else per-element cp.async; 1 = always per-element cp.async.
                             Same data, same arithmetic. */
+  int record_layout;     /* plain update kernel (REDs, no replica): 1 = the record layout -- each
+                            coordinate is a 32-byte record {x_v, abar_v, D_v, .} (D_v = n/n_v,
+                            PAPER.md:108-110) and the gather of an entry returns D_v with x and
+                            abar from the same sector: no per-entry D array (nnz x 8 bytes) and
+                            no expand pass per reload; the hot split's features are found in a
+                            per-block shared-memory table.  Measured slower on c3 / c4 (two
+                            loads per entry on the popular lines).
+                            0 (default) = D_{c_k} streamed with the row from a per-entry copy.
+                            Same arithmetic. */
 } asaga_options;
 
 typedef struct {
@@ -191,6 +200,9 @@ typedef struct {
   int64_t combine_passes; /* communication-warp passes, summed over blocks, of the last run
                              (pass period = last_run_ms * combine_blocks / combine_passes) */
   int combine_cluster;    /* blocks per cluster of the combine kernel */
+  int record_layout;      /* 1 when asaga_run uses the record layout (option record_layout, the
+                             plain kernel with REDs and no replica) */
+  int hot_table_slots;    /* the record layout's hot-split table (0 = none) */
 } asaga_stats_t;
 
 /* Fill *opt with the defaults listed above. */

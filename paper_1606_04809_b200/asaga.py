@@ -49,7 +49,8 @@ class Options(ctypes.Structure):
                 ("combine_cluster", ctypes.c_int), ("combine_write_through", ctypes.c_int),
                 ("combine_max_blocks", ctypes.c_int), ("l2_persist_state", ctypes.c_int),
                 ("pipe_late_min_freq", ctypes.c_double), ("pipe_merge_ns", ctypes.c_int),
-                ("row_copy_elementwise", ctypes.c_int)]
+                ("row_copy_elementwise", ctypes.c_int),
+                ("record_layout", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -64,7 +65,8 @@ class Stats(ctypes.Structure):
                 ("algorithm", ctypes.c_int), ("hot_split_min_freq", ctypes.c_double),
                 ("smem_replica", ctypes.c_int), ("combine_hot", ctypes.c_int),
                 ("combine_blocks", ctypes.c_int), ("combine_passes", ctypes.c_int64),
-                ("combine_cluster", ctypes.c_int)]
+                ("combine_cluster", ctypes.c_int), ("record_layout", ctypes.c_int),
+                ("hot_table_slots", ctypes.c_int)]
 
 
 ABI_FUNCTIONS = {
@@ -181,7 +183,8 @@ class Asaga:
                  combine_min_freq: float = 0.0, combine_cluster: int = 0,
                  combine_write_through: bool = False, combine_max_blocks: int = 0,
                  l2_persist_state: bool = False, pipe_late_min_freq: float = 0.0,
-                 pipe_merge_ns: int = 0, row_copy_elementwise: bool = False):
+                 pipe_merge_ns: int = 0, row_copy_elementwise: bool = False,
+                 record_layout: bool = False):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -211,6 +214,7 @@ class Asaga:
         opt.pipe_late_min_freq = float(pipe_late_min_freq)
         opt.pipe_merge_ns = int(pipe_merge_ns)
         opt.row_copy_elementwise = int(bool(row_copy_elementwise))
+        opt.record_layout = int(bool(record_layout))
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

@@ -96,6 +96,9 @@ struct asaga_ctx {
   int l2_persist = 0;          // plain kernel: L2 access-policy window (persisting) over xa
   double pipe_freq = 0.0;      // > 0: asaga_pipe_kernel, features with p_v >= it read late
   int row_copy_elementwise = 0;  // plain kernel: per-element cp.async row staging (no TMA bulk)
+  int rec_layout = 0;            // plain kernel: the record layout (D from the coordinate record, no dv stream)
+  int32_t* hot_tab = nullptr;    // record layout + hot split: membership table of the hot-split features
+  int hot_log = 0;               // ... log2 of its slots
   int comb_wt = 0;             // write-through (replica reads only)
   bool shape_valid = false;    // launch shape computed for shape_key
   int64_t row_cap = 0;         // longest row the launch shape holds (nr * lanes + overflow)
@@ -242,25 +245,27 @@ using UpdFn = void (*)(UpdateParams);
 template <int G, int NR, bool DET, bool REPL>
 UpdFn pick_mode(int mode) {
   switch (mode) {
-    case 0: return asaga_update_kernel<G, NR, DET, 0, REPL>;
-    case 2: return asaga_update_kernel<G, NR, DET, 2, REPL>;
-    default: return asaga_update_kernel<G, NR, DET, 1, REPL>;
+    case 0: return asaga_update_kernel<G, NR, DET, 0, REPL, false>;
+    case 2: return asaga_update_kernel<G, NR, DET, 2, REPL, false>;
+    default: return asaga_update_kernel<G, NR, DET, 1, REPL, false>;
   }
 }
 
 template <int G, int NR>
-UpdFn pick_upd(bool det, int mode, bool repl) {
+UpdFn pick_upd(bool det, int mode, bool repl, bool rec) {
+  if (rec)  // record layout (MODE 1, no replica)
+    return det ? asaga_update_kernel<G, NR, true, 1, false, true> : asaga_update_kernel<G, NR, false, 1, false, true>;
   if (det) return pick_mode<G, NR, true, false>(mode);  // deterministic mode reads L2 directly
   return repl ? pick_mode<G, NR, false, true>(mode) : pick_mode<G, NR, false, false>(mode);
 }
 
 template <int G>
-UpdFn pick_upd_nr(int nr, bool det, int mode, bool repl) {
+UpdFn pick_upd_nr(int nr, bool det, int mode, bool repl, bool rec) {
   switch (nr) {
-    case 1: return pick_upd<G, 1>(det, mode, repl);
-    case 2: return pick_upd<G, 2>(det, mode, repl);
-    case 4: return pick_upd<G, 4>(det, mode, repl);
-    default: return pick_upd<G, 8>(det, mode, repl);
+    case 1: return pick_upd<G, 1>(det, mode, repl, rec);
+    case 2: return pick_upd<G, 2>(det, mode, repl, rec);
+    case 4: return pick_upd<G, 4>(det, mode, repl, rec);
+    default: return pick_upd<G, 8>(det, mode, repl, rec);
   }
 }
 
@@ -269,6 +274,7 @@ int scatter_mode(const asaga_ctx* ctx);
 
 bool use_replica(const asaga_ctx* ctx);
 bool use_pipe(const asaga_ctx* ctx);
+bool use_rec(const asaga_ctx* ctx);
 UpdFn pipe_fn(const asaga_ctx* ctx, int lanes, int nr);
 
 UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
@@ -276,10 +282,11 @@ UpdFn update_fn(const asaga_ctx* ctx, int lanes, int nr) {
   const bool det = ctx->deterministic != 0;
   const int mode = scatter_mode(ctx);
   const bool repl = use_replica(ctx);
+  const bool rec = use_rec(ctx);
   switch (lanes) {
-    case 8: return pick_upd_nr<8>(nr, det, mode, repl);
-    case 16: return pick_upd_nr<16>(nr, det, mode, repl);
-    default: return pick_upd_nr<32>(nr, det, mode, repl);
+    case 8: return pick_upd_nr<8>(nr, det, mode, repl, rec);
+    case 16: return pick_upd_nr<16>(nr, det, mode, repl, rec);
+    default: return pick_upd_nr<32>(nr, det, mode, repl, rec);
   }
 }
 
@@ -440,6 +447,22 @@ int scatter_mode(const asaga_ctx* ctx) {
   return ctx->bulk_dmax > 0.0 ? 2 : 1;
 }
 
+// The record layout (asaga_update_kernel<REC>): D_v read from the 32-byte coordinate record
+// {x_v, abar_v, D_v, .} with the gather itself (no per-entry D stream, no expand pass).
+// The plain kernel with REDs and no replica, S >= 2, and (hot split) a membership table.
+bool use_rec(const asaga_ctx* ctx) {
+  return ctx->rec_layout && !use_pipe(ctx) && !use_combine(ctx) && scatter_mode(ctx) == 1 && !use_replica(ctx) &&
+         ctx->S >= 2 && (ctx->hot_dmax == 0.0 || ctx->hot_tab != nullptr);
+}
+size_t rec_tab_bytes(const asaga_ctx* ctx) {  // the kernel's shared copy of the table
+  return ctx->hot_tab != nullptr ? (size_t)sizeof(int32_t) << ctx->hot_log : 0;
+}
+// shared memory ahead of the worker groups: the replica, or the record layout's table
+// (reserved whenever the table exists: set_algorithm may switch the kernel later)
+size_t pre_bytes(const asaga_ctx* ctx, bool launch) {
+  return replica_bytes(ctx) + ((!launch || use_rec(ctx)) && ctx->rec_layout ? rec_tab_bytes(ctx) : 0);
+}
+
 // Spread `workers` groups over all SMs: the smallest power-of-two block (>= one
 // warp, <= kBlock threads) that still gives every SM a block.  Workers packed
 // onto few SMs queue behind each other's row copies and REDs in the SM's LSU
@@ -540,11 +563,11 @@ asaga_status configure_update(asaga_ctx* ctx) {
   const int comm = mg ? 32 : 0;
   int tpb_max = kBlock - comm;
   while (tpb_max > 32 &&
-         replica_bytes(ctx) + (size_t)(tpb_max / lanes) * group_bytes + merge_bytes(ctx, tpb_max / lanes) > 226 * 1024)
+         pre_bytes(ctx, false) + (size_t)(tpb_max / lanes) * group_bytes + merge_bytes(ctx, tpb_max / lanes) > 226 * 1024)
     tpb_max = mg ? tpb_max - 32 : tpb_max / 2;
   ctx->max_tpb = tpb_max;
   const int gpb = tpb_max / lanes;
-  ctx->smem = replica_bytes(ctx) + (size_t)gpb * group_bytes + merge_bytes(ctx, gpb);
+  ctx->smem = pre_bytes(ctx, false) + (size_t)gpb * group_bytes + merge_bytes(ctx, gpb);
   UpdFn fn = update_fn(ctx, lanes, nr);
   if (ctx->smem > 226 * 1024)
     return fail(ctx, ASAGA_E_INVALID_ARG, "row of %lld entries too long for the update kernel",
@@ -571,14 +594,27 @@ asaga_status alloc_state(asaga_ctx* ctx) {
   // Small d (every feature hot, e.g. c2's d = 54): give every feature its own
   // 1 KiB block so hot features spread over L2 slices (2.2x at 1024 in flight,
   // profiles/r01_update_kernel.md); larger d keeps pairs dense (S = 8 measured no gain on c3).
-  ctx->S = d <= 4096 ? 64 : 1;
+  // Larger d: dense 16-byte pairs, or 32-byte records {x_v, abar_v, D_v, .} (S = 2) for the
+  // record layout.
+  ctx->S = d <= 4096 ? 64 : (ctx->rec_layout ? 2 : 1);
 #ifdef ASAGA_TIMING
   if (const char* e = getenv("ASAGA_PAIR_STRIDE")) ctx->S = std::max(1, atoi(e));  // experiments
 #endif
   TRY(dalloc(ctx, &ctx->xa, (size_t)d * ctx->S));
   TRY(dalloc(ctx, &ctx->D, d));
   TRY(dalloc(ctx, &ctx->habar, d));
-  TRY(dalloc(ctx, &ctx->dv, nnz));
+  // (dv, D per stored entry: allocated by the first expand -- the record layout needs none)
+  if (ctx->hot_dmax > 0.0 && ctx->S >= 2 && ctx->rec_layout) {
+    // hot-split table: the features with D_v <= hot_dmax number at most nnz/n x hot_dmax
+    // (sum_v n_v = nnz) and at most d; >= 8 slots per such feature keep the linear probes short
+    const double hmax = std::min((n > 0 ? (double)nnz / (double)n : 0.0) * ctx->hot_dmax, (double)d) + 8.0;
+    int log = 8;
+    while (log < 14 && (double)(1 << log) < 8.0 * hmax) ++log;
+    if ((double)(1 << log) >= 8.0 * hmax) {  // else (> 16K slots): the dv stream carries the split
+      TRY(dalloc(ctx, &ctx->hot_tab, (size_t)1 << log));
+      ctx->hot_log = log;
+    }
+  }
   TRY(dalloc(ctx, &ctx->alpha, n));
   TRY(dalloc(ctx, &ctx->counts, d));
   TRY(dalloc(ctx, &ctx->tmp_n, n));
@@ -729,12 +765,17 @@ asaga_status ingest_enqueue(asaga_ctx* ctx, const int64_t* indptr_in, const int3
   ip.row_cap = ctx->row_cap;
   ip.hot_expected = ctx->hot_freq > 0.0 ? ctx->comb_H : -1;
   ip.guard = guard ? 1 : 0;
+  ip.hot_tab = ctx->hot_tab;
+  ip.hot_log = ctx->hot_log;
+  ip.hot_dmax = ctx->hot_dmax;
+  if (ctx->hot_tab) CK(ctx, cudaMemsetAsync(ctx->hot_tab, 0xff, sizeof(int32_t) << ctx->hot_log, ctx->stream));
   ctx->ing_fused = ip.fuse != 0;
   void* iargs[] = {&ip};
   CK(ctx, cudaLaunchKernel(kfn, dim3(grid), dim3(kIngestBlock), iargs, hsmem, ctx->stream));
   if (!ip.fuse) {
-    profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(ctx->counts, ctx->xa, ctx->S, ctx->habar,
-                                                                          ctx->D, d, n, ctx->flag + 1);
+    profile_kernel<<<grid_for(ctx, d, kBlock), kBlock, 0, ctx->stream>>>(
+        ctx->counts, ctx->xa, ctx->S, ctx->habar, ctx->D, d, n, ctx->flag + 1, ctx->hot_tab, ctx->hot_log,
+        ctx->hot_dmax);
     CK(ctx, cudaGetLastError());
   }
   if (ctx->hot_freq > 0.0 && !ip.fuse) {  // hot set (combine kernel / pipe merge): p_v >= hot_freq
@@ -764,7 +805,9 @@ asaga_status enqueue_report(asaga_ctx* ctx, bool guard) {
 
 // D per stored entry: read by the plain kernel and by the combine kernel unless every feature
 // is hot (D from its block table); the pipelined kernel gathers D_v from the d-vector itself
-bool needs_dv(const asaga_ctx* ctx) { return !(use_combine(ctx) && ctx->comb_H == ctx->d) && !use_pipe(ctx); }
+bool needs_dv(const asaga_ctx* ctx) {
+  return !(use_combine(ctx) && ctx->comb_H == ctx->d) && !use_pipe(ctx) && !use_rec(ctx);
+}
 
 // D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
 // with every feature hot (which reads D from its block table) streams it with the row
@@ -772,6 +815,7 @@ bool needs_dv(const asaga_ctx* ctx) { return !(use_combine(ctx) && ctx->comb_H =
 // matrix has not been expanded -- e.g. after set_algorithm leaves the pipelined kernel)
 asaga_status enqueue_expand(asaga_ctx* ctx) {
   if (!needs_dv(ctx)) return ASAGA_OK;
+  if (!ctx->dv) TRY(dalloc(ctx, &ctx->dv, ctx->nnz));
   expand_d_kernel<<<grid_for(ctx, ctx->nnz, kBlock), kBlock, 0, ctx->stream>>>(
       ctx->cols, ctx->D, ctx->nnz, ctx->hot_dmax, ctx->dv, ctx->slot_of, ctx->flag + 2, ctx->d, ctx->eslot);
   CK(ctx, cudaGetLastError());
@@ -970,6 +1014,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   }
   ctx->pipe_merge = o.pipe_merge_ns;
   ctx->row_copy_elementwise = o.row_copy_elementwise ? 1 : 0;
+  ctx->rec_layout = o.record_layout ? 1 : 0;
   ctx->hot_freq = o.combine_min_freq > 0.0 ? o.combine_min_freq : (ctx->pipe_merge ? ctx->pipe_freq : 0.0);
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
   *ctx_out = ctx;
@@ -1141,7 +1186,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.cols = ctx->cols;
   p.vals = ctx->vals;
   p.y = ctx->y;
-  p.dv = ctx->dv;
+  p.dv = use_rec(ctx) ? nullptr : ctx->dv;
   p.D = ctx->D;
   p.xa = ctx->xa;
   p.S = ctx->S;
@@ -1182,8 +1227,10 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   // 1-D TMA row staging when the arrays the kernel streams are 16-B aligned (the caller's
   // borrowed arrays may be offset views)
   p.nnz = ctx->nnz;
-  p.bulk_rows = ((((uintptr_t)ctx->cols) | ((uintptr_t)ctx->vals) | ((uintptr_t)ctx->dv)) & 15) == 0 &&
+  p.bulk_rows = ((((uintptr_t)ctx->cols) | ((uintptr_t)ctx->vals) | ((uintptr_t)p.dv)) & 15) == 0 &&
                 !ctx->row_copy_elementwise;
+  p.hot_tab = use_rec(ctx) && ctx->hot_dmax > 0.0 ? ctx->hot_tab : nullptr;
+  p.hot_log = ctx->hot_log;
   p.ok = ctx->flag + 3;  // 0 while an asynchronous reload's data does not fit this launch
   if (needs_dv(ctx) && !ctx->dv_ready) TRY(enqueue_expand(ctx));
   if (p.comm_passes && use_combine(ctx))
@@ -1219,7 +1266,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   int grid = 1, block = 32;
   launch_shape(ctx, workers, &grid, &block);
   const int groups = (block - (use_merge(ctx) ? 32 : 0)) / ctx->lanes;
-  const size_t smem = replica_bytes(ctx) + (size_t)groups * ctx->group_bytes + merge_bytes(ctx, groups);
+  const size_t smem = pre_bytes(ctx, true) + (size_t)groups * ctx->group_bytes + merge_bytes(ctx, groups);
   CK(ctx, ensure_smem_attr(ctx->device, (const void*)fn, (int)smem));
   if (timed) CK(ctx, cudaEventRecord(ctx->ev0, ctx->stream));
   if (ctx->l2_persist) {
@@ -1283,6 +1330,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->pipe_late_min_freq = 0.0;
   opt->pipe_merge_ns = 0;
   opt->row_copy_elementwise = 0;
+  opt->record_layout = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,
@@ -1626,6 +1674,8 @@ asaga_status asaga_stats(const asaga_ctx* cctx, asaga_stats_t* out) {
   out->combine_hot = use_combine(ctx) ? ctx->comb_H : 0;
   out->combine_blocks = use_combine(ctx) ? ctx->grid : 0;
   out->combine_cluster = use_combine(ctx) ? ctx->comb_csize : 0;
+  out->record_layout = use_rec(ctx) ? 1 : 0;
+  out->hot_table_slots = ctx->hot_tab != nullptr ? 1 << ctx->hot_log : 0;
   out->combine_passes = 0;
   if (use_combine(ctx)) {
     unsigned long long c = 0;

@@ -97,6 +97,61 @@ __device__ __forceinline__ double2 ld_na2(const double2* p) {
 #endif
   return v;
 }
+// The 32-byte coordinate record {x_v, abar_v, D_v, .} (S >= 2): the {x, abar} pair and D_v
+// in ONE sector, gathered by a 128-bit and a 64-bit load (D_v is never written after A1)
+// -- D needs no per-entry stream.  (A single 256-bit load, LDG.E.NA.ENL2.256 on
+// sm_100, of the record was measured to break ASAGA's convergence on c3 -- f - f* stalls
+// at ~1e-4 with the hot split, with or without .STRONG.GPU -- while the deterministic
+// parity held: those loads are not used; profiles/r02_update_kernel.md.)
+struct Rec3 {
+  double x, ab, D;
+};
+__device__ __forceinline__ Rec3 ld_na_rec(const double2* p) {
+  const double2 a = ld_na2(p);
+  Rec3 r;
+  r.x = a.x;
+  r.ab = a.y;
+  r.D = ld_na(&p[1].x);
+  return r;
+}
+
+// Hot-split membership table (record layout with hot_split_min_freq): the features with
+// 0 < D_v <= hot_dmax, open addressing with linear probing in 2^log slots (-1 = free),
+// filled to at most 1/8 by construction (asaga.cu: slots >= 8 x the bound
+// nnz/n x hot_dmax on their number).  Membership is exact whatever the insertion order.
+__device__ __forceinline__ unsigned hot_hash(int v, int log) {
+  return ((unsigned)v * 0x9E3779B1u) >> (32 - log);
+}
+__device__ __forceinline__ void hot_insert(int32_t* tab, int log, int v) {
+  const unsigned mask = (1u << log) - 1u;
+  for (unsigned h = hot_hash(v, log);; h = (h + 1u) & mask) {
+    const int prev = atomicCAS(tab + h, -1, v);
+    if (prev == -1 || prev == v) return;
+  }
+}
+__device__ __forceinline__ bool hot_lookup(const int32_t* tab, int log, int c) {
+  const unsigned mask = (1u << log) - 1u;
+  unsigned h = hot_hash(c, log);
+  int e = tab[h];
+  while (e != c && e != -1) {
+    h = (h + 1u) & mask;
+    e = tab[h];
+  }
+  return e == c;
+}
+// A1: coordinate v's state init (x = abar = 0), D_v, its record copy (S >= 2) and its
+// hot-table entry
+__device__ __forceinline__ void init_coord(int64_t v, int cnt, int64_t n, double2* __restrict__ xa, int S,
+                                           double* __restrict__ habar, double* __restrict__ D,
+                                           int32_t* __restrict__ hot_tab, int hot_log, double hot_dmax) {
+  const double Dv = cnt > 0 ? (double)n / (double)cnt : 0.0;
+  xa[v * S] = make_double2(0.0, 0.0);
+  if (S >= 2) xa[v * S + 1] = make_double2(Dv, 0.0);
+  habar[v] = 0.0;
+  D[v] = Dv;
+  if (hot_tab != nullptr && Dv > 0.0 && Dv <= hot_dmax) hot_insert(hot_tab, hot_log, (int)v);
+}
+
 __device__ __forceinline__ void st_cg(double* p, double v) {
   asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -233,6 +288,9 @@ struct IngestParams {
   int self_init;
   int32_t* part;
   double* alpha;
+  int32_t* hot_tab;       // record layout's hot-split table (pre-set to -1), or NULL
+  int hot_log;
+  double hot_dmax;
 };
 
 // ---------------------------------------------------------------------------
@@ -275,7 +333,8 @@ __device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ c
                      double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
                      int* __restrict__ max_count, double comb_dmax, int max_h,
                      int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
-                     int* __restrict__ n_hot);
+                     int* __restrict__ n_hot, int32_t* __restrict__ hot_tab,
+                     int hot_log, double hot_dmax);
 __device__ __forceinline__ void report_body(const unsigned long long* __restrict__ scratch,
                                             int* __restrict__ flag, unsigned long long* host_out,
                                             int64_t row_cap, int hot_expected, int guard);
@@ -559,7 +618,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         __syncthreads();
       }
       profile_small_body(p.counts, p.xa, p.S, p.habar, p.D, (int)p.d, p.n, p.flag + 1, p.comb_dmax, p.max_h,
-                         p.slot_of, p.hot_id, p.flag + 2);
+                         p.slot_of, p.hot_id, p.flag + 2, p.hot_tab, p.hot_log, p.hot_dmax);
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -578,14 +637,13 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
 // A1 finish: D_v = n / n_v (IEEE division, reading R4), state init, Delta_r.
 __global__ void profile_kernel(const int32_t* __restrict__ counts, double2* __restrict__ xa,
                                int S, double* __restrict__ habar, double* __restrict__ D, int64_t d,
-                               int64_t n, int* __restrict__ max_count) {
+                               int64_t n, int* __restrict__ max_count, int32_t* __restrict__ hot_tab,
+                               int hot_log, double hot_dmax) {
   int my = 0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < d;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int c = counts[v];
-    xa[v * S] = make_double2(0.0, 0.0);
-    habar[v] = 0.0;
-    D[v] = c > 0 ? (double)n / (double)c : 0.0;
+    init_coord(v, c, n, xa, S, habar, D, hot_tab, hot_log, hot_dmax);
     my = max(my, c);
   }
   for (int off = 16; off > 0; off >>= 1) my = max(my, __shfl_xor_sync(0xffffffffu, my, off));
@@ -676,7 +734,8 @@ __device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ c
                      double* __restrict__ habar, double* __restrict__ D, int d, int64_t n,
                      int* __restrict__ max_count, double comb_dmax, int max_h,
                      int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_id,
-                     int* __restrict__ n_hot) {
+                     int* __restrict__ n_hot, int32_t* __restrict__ hot_tab,
+                     int hot_log, double hot_dmax) {
   __shared__ int warp_tot[32];
   __shared__ int warp_max[32];
   constexpr int PER = 4;  // features per thread (d <= 4096)
@@ -689,9 +748,7 @@ __device__ __forceinline__ void profile_small_body(const int32_t* __restrict__ c
     if (v < d) {
       const int c = counts[v];
       const double Dv = c > 0 ? (double)n / (double)c : 0.0;
-      xa[(int64_t)v * S] = make_double2(0.0, 0.0);
-      habar[v] = 0.0;
-      D[v] = Dv;
+      init_coord(v, c, n, xa, S, habar, D, hot_tab, hot_log, hot_dmax);
       mx = max(mx, c);
       flag[q] = (comb_dmax > 0.0 && Dv > 0.0 && Dv <= comb_dmax) ? 1 : 0;
       mine += flag[q];
@@ -829,6 +886,10 @@ struct UpdateParams {
                           // 16-B aligned); 0 = per-element cp.async
   int64_t nnz;            // stored entries (bulk copies never read past them)
   const int* ok;          // run guard: 0 = skip (an asynchronous reload's data does not fit)
+  // asaga_update_kernel<REC>: D_v from the 32-byte record (no dv stream); hot split by
+  // membership in hot_tab (2^hot_log slots, copied to shared memory), NULL = no split
+  const int32_t* hot_tab;
+  int hot_log;
 };
 
 // Shared memory per group: a P-entry {dx, dabar} source buffer for the TMA bulk
@@ -900,7 +961,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // Row staging of the plain update kernel: the first P entries of the row (values, D per
-// entry, columns) into a stage.  bulk: lane 0 issues three 1-D TMA copies of the 16-B
+// entry unless dv is NULL -- the record layout --, columns) into a stage.  bulk: lane 0 issues three 1-D TMA copies of the 16-B
 // aligned supersets (UBLKCP: three instructions per row instead of 3 ceil(len/G) LDGSTS per
 // lane), completing on the stage's mbarrier; otherwise (misaligned caller arrays, or the
 // last rows, whose aligned superset would read past nnz) per-element cp.async, and lane 0
@@ -921,14 +982,16 @@ __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, c
   const int64_t hs = hi - lo > P ? lo + P : hi;  // staged entries [lo, hs)
   const int64_t lo_c = lo & ~(int64_t)3, hi_c = (hs + 3) & ~(int64_t)3;
   const int64_t lo_v = lo & ~(int64_t)1, hi_v = (hs + 1) & ~(int64_t)1;
+  // (the caller has synchronised the group since the previous sample's scatter read the
+  // stage this copy overwrites: asaga_update_kernel's loop top)
   if (bulk && hi_c <= nnz && hi_v <= nnz) {  // group-uniform
     if (g == 0) {
       const unsigned bc = (unsigned)((hi_c - lo_c) * 4), bv = (unsigned)((hi_v - lo_v) * 8);
       fence_proxy_async_smem();  // earlier generic reads of this stage before the async writes
-      mbar_arrive_tx(bar, bc + 2 * bv);
+      mbar_arrive_tx(bar, bc + (dv != nullptr ? 2 : 1) * bv);
       bulk_g2s(sc, cols + lo_c, bc, bar, pol);
       bulk_g2s(sv, vals + lo_v, bv, bar, pol);
-      bulk_g2s(sd, dv + lo_v, bv, bar, pol);
+      if (dv != nullptr) bulk_g2s(sd, dv + lo_v, bv, bar, pol);
     }
   } else {
     const int len = (int)(hs - lo);
@@ -940,7 +1003,7 @@ __device__ __forceinline__ void issue_row_copy(unsigned char* base, int stage, c
       if (j * G + g < len) {
         cp_async4_ef(sc + oc + j * G + g, cols + k, pol);
         cp_async8_ef(sv + ov + j * G + g, vals + k, pol);
-        cp_async8_ef(sd + ov + j * G + g, dv + k, pol);
+        if (dv != nullptr) cp_async8_ef(sd + ov + j * G + g, dv + k, pol);
       }
     }
     if (g == 0) mbar_arrive(bar);  // (the data is waited for with cp.async.wait_all)
@@ -975,9 +1038,16 @@ __device__ unsigned long long g_phase_cycles[12];
 // replica entries from L2 every repl_every samples, so a replica value is a past value of
 // the shared state of bounded age: the reads stay the paper's inconsistent reads (P:137,
 // P:266-268) with a larger, still bounded, overlap (Assumption 1).
-template <int G, int NR, bool DET, int MODE, bool REPL>
-__global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
+// REC (record layout, MODE 1, no replica): D_v comes with the gather of the 32-byte
+// coordinate record (no per-entry D stream, no expand pass); a hot-split entry is found
+// in the block's shared copy of the membership table.
+// (REC keeps x, abar, D and a hot entry's abar of every chunk in flight: 8 registers per
+// chunk instead of 4, so one resident 256-thread block per SM -- 8 samples, beyond the
+// ~3 per SM the convergent concurrency asks for -- and no spills at NR = 8)
+template <int G, int NR, bool DET, int MODE, bool REPL, bool REC>
+__global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdateParams p) {
   constexpr bool ATOMIC = MODE != 0;
+  static_assert(!REC || (MODE == 1 && !REPL), "record layout: REDs, no replica");
   if (p.ok != nullptr && *reinterpret_cast<const volatile int*>(p.ok) == 0) return;  // run guard
 #ifdef ASAGA_TIMING
   unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -993,11 +1063,18 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   // as many workers as SMs every SM runs some (launch_shape puts one block on each)
   const int64_t w = (int64_t)(threadIdx.x / G) * gridDim.x + blockIdx.x;
   double2* rx = reinterpret_cast<double2*>(smem_raw);  // REPL replica (first in smem)
-  const size_t repl_bytes = REPL ? (((size_t)p.repl_d * sizeof(double2) + 15) & ~(size_t)15) : 0;
+  const size_t repl_bytes = REPL ? (((size_t)p.repl_d * sizeof(double2) + 15) & ~(size_t)15)
+                            : (REC && p.hot_tab != nullptr) ? ((size_t)sizeof(int32_t) << p.hot_log) : 0;
   if (REPL) {  // fill before any early exit: the whole block takes part in the barrier
     for (int v = threadIdx.x; v < p.repl_d; v += blockDim.x) rx[v] = ld_na2(p.xa + (int64_t)v * p.S);
     __syncthreads();
   }
+  int32_t* ht = reinterpret_cast<int32_t*>(smem_raw);  // REC: the hot-split table (first in smem)
+  if (REC && p.hot_tab != nullptr) {
+    for (int q = threadIdx.x; q < (1 << p.hot_log); q += blockDim.x) ht[q] = __ldg(p.hot_tab + q);
+    __syncthreads();
+  }
+  const double* const dvs = REC ? nullptr : p.dv;  // the row stream's D (not with REC)
   if (w >= p.workers) return;
   unsigned char* gbase =
       smem_raw + repl_bytes + (size_t)(threadIdx.x / G) * GroupSmem<G, NR>::bytes(p.overflow);
@@ -1038,7 +1115,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
   int64_t i = sample_of(0);
   int64_t lo = __ldg(&p.rowptr[i]), hi = __ldg(&p.rowptr[i + 1]);
   int stage = 0;
-  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, p.dv, p.y + i, lo, hi, g, p.bulk_rows, p.nnz);
+  issue_row_copy<G, NR>(gbase, stage, p.cols, p.vals, dvs, p.y + i, lo, hi, g, p.bulk_rows, p.nnz);
   int64_t in1 = 0, lo1 = 0, hi1 = 0, in2 = 0;
   in1 = sample_of(1);
   in2 = sample_of(2);
@@ -1062,6 +1139,17 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     unsigned char* sbase = gbase + GS::delta_bytes + stage * GS::stage_bytes;
     mbar_wait(sbase + GS::mbar_off, (phase_bits >> stage) & 1u);
     phase_bits ^= 1u << stage;
+    // The group synchronises here: (1) b_i is lane 0's cp.async (the mbarrier tracks the
+    // bulk bytes only, and lane 0 arrives before its per-element copies land), so the other
+    // lanes may read it only after lane 0's wait above; (2) this iteration's look-ahead copy
+    // overwrites the stage the previous sample scattered from, slots other lanes read (the
+    // bulk path writes the whole stage from lane 0; a row at another 16-B offset shifts every
+    // slot of the per-element path).  Nothing else orders the group's lanes between that
+    // scatter and here: without it, c3 at its operating point plateaued at f - f* ~ 1e-4
+    // once the record layout changed the code's timing (a stale b_i flips a lane's signs).
+#ifndef ASAGA_NO_GROUP_SYNC  // (measurement variant only)
+    __syncwarp(gmask);
+#endif
     TMARK(0);
     const double* sv = reinterpret_cast<const double*>(sbase + GS::vals_off) + (lo & 1);
     const double* sd = reinterpret_cast<const double*>(sbase + GS::dv_off) + (lo & 1);
@@ -1072,6 +1160,34 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     // gathers of x^, abar^ and D for every resident chunk are issued before any use
     double qq[NR];
     double2 xb[NR];
+    double Dr[NR], hb[NR];  // REC: D_c from the record; abar_c of a hot-split entry
+    unsigned hm = 0;        // REC: bit j = chunk j's entry is hot-split
+    if (REC) {
+      // every record gather first, then the table lookups and the hot entries' abar gathers
+      // (separate registers: no load waits on another in-flight load's destination)
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (j * G >= len) break;  // group-uniform
+        if (j * G + g < len) {
+          const Rec3 r = ld_na_rec(p.xa + (int64_t)sc[j * G + g] * p.S);
+          xb[j] = make_double2(r.x, r.ab);
+          Dr[j] = r.D;
+        }
+      }
+      if (p.hot_tab != nullptr) {
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          if (j * G >= len) break;  // group-uniform
+          if (j * G + g < len) {
+            const int c = sc[j * G + g];
+            if (hot_lookup(ht, p.hot_log, c)) {
+              hb[j] = ld_na(p.habar + c);
+              hm |= 1u << j;
+            }
+          }
+        }
+      }
+    } else
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       if (j * G >= len) break;  // group-uniform
@@ -1115,7 +1231,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
     constexpr bool copy_late = false;
 #endif
     if (has1 && !copy_late)
-      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
+      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, dvs, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
     int64_t lo2 = 0, hi2 = 0;
     if (has2) {
       lo2 = __ldg(&p.rowptr[in2]);
@@ -1128,13 +1244,24 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const int64_t k = lo + j * G + g;
       if (j * G + g < len) {
         dot = fma(sv[j * G + g], xb[j].x, dot);
-        qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
+        if (REC)
+          qq[j] = Dr[j] * fma(p.lambda_, xb[j].x, ((hm >> j) & 1u) ? hb[j] : xb[j].y);
+        else
+          qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
       }
     }
     if (len > P)  // group-uniform: long rows only
     for (int64_t k = lo + P + g; k < hi; k += G) {
       const int c = ld_nc_i32(p.cols + k);
       const double a = ld_nc_f64(p.vals + k);
+      if (REC) {
+        const Rec3 r = ld_na_rec(p.xa + (int64_t)c * p.S);
+        const bool hot = p.hot_tab != nullptr && hot_lookup(ht, p.hot_log, c);
+        const double ab = hot ? ld_na(p.habar + c) : r.ab;
+        dot = fma(a, r.x, dot);
+        qs[k - lo - P] = r.D * fma(p.lambda_, r.x, ab);
+        continue;
+      }
       const double Dv = ld_nc_f64(p.dv + k);
       const double2 v = REPL ? rx[c]
                         : Dv < 0.0 ? make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c))
@@ -1143,7 +1270,7 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       qs[k - lo - P] = fabs(Dv) * fma(p.lambda_, v.x, v.y);
     }
     if (has1 && copy_late)
-      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, p.dv, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
+      issue_row_copy<G, NR>(gbase, stage ^ 1, p.cols, p.vals, dvs, p.y + in1, lo1, hi1, g, p.bulk_rows, p.nnz);
     TMARK(1);
     // ---- scalar derivative (folded logistic) and memory difference
     dot = group_sum<G>(dot, gmask) * yb;  // folded margin b_i a_i . x^ (exact: b = +-1)
@@ -1172,7 +1299,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
         const double a = sv[j * G + g];
         const double u = fma(db, a, qq[j]);
         double* xv = &p.xa[(int64_t)c * p.S].x;
-        double* abv = (p.split && sd[j * G + g] < 0.0) ? p.habar + c : xv + 1;  // hot split
+        double* abv = REC ? (((hm >> j) & 1u) ? p.habar + c : xv + 1)
+                          : (p.split && sd[j * G + g] < 0.0) ? p.habar + c : xv + 1;  // hot split
         if (MODE == 2 && sd[j * G + g] <= p.bulk_dmax) {
           dbuf[j * G + g] = make_double2(ngam * u, p.frozen ? 0.0 : db * a * p.inv_n);
         } else if (MODE >= 1) {
@@ -1211,7 +1339,8 @@ __global__ void __launch_bounds__(256, 2) asaga_update_kernel(UpdateParams p) {
       const double a = ld_nc_f64(p.vals + k);
       const double u = fma(db, a, qs[k - lo - P]);
       double* xv = &p.xa[(int64_t)c * p.S].x;
-      double* abv = ld_nc_f64(p.dv + k) < 0.0 ? p.habar + c : xv + 1;  // hot split
+      const bool hot = REC ? (p.hot_tab != nullptr && hot_lookup(ht, p.hot_log, c)) : ld_nc_f64(p.dv + k) < 0.0;
+      double* abv = hot ? p.habar + c : xv + 1;  // hot split
       if (ATOMIC) {
         red_add(xv, ngam * u);
         if (!p.frozen) red_add(abv, db * a * p.inv_n);

@@ -49,7 +49,7 @@ def test_binding_matches_header(libpath):
     from paper_1606_04809_b200 import asaga
 
     assert set(asaga.ABI_FUNCTIONS) == set(declared())
-    assert asaga.lib().asaga_abi_version() == 2
+    assert asaga.lib().asaga_abi_version() == 3
     assert asaga.lib().asaga_status_string(6) == b"ASAGA_E_DIVERGED"
     assert asaga.lib().asaga_last_error(None)  # never NULL
 

@@ -128,12 +128,17 @@ def test_sigma_device_function_accuracy():
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
-def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False):
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False, record=False):
     m = asaga_mod()
     g = gamma_of(prob)
     a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
                              bulk_scatter_min_freq=bulk, hot_split_min_freq=split,
-                             row_copy_elementwise=elementwise)
+                             row_copy_elementwise=elementwise, record_layout=record)
+    st = a.stats()
+    if not record or bulk > 0.0:
+        assert st["record_layout"] == 0
+    else:  # (a hot set too large for the shared-memory table keeps the per-entry D stream)
+        assert st["record_layout"] == 1 or (split > 0.0 and st["hot_table_slots"] == 0 and prob.d > 2048)
     st = oracle.State(prob.n, prob.d)
     D = oracle.reweight(prob.n, oracle.column_counts(prob))
     done = 0
@@ -181,6 +186,18 @@ def test_deterministic_bulk_scatter(name, bulk):
 def test_deterministic_hot_split(name, split):
     """abar of popular features in its own array (x and abar on separate lines): same arithmetic."""
     _det_compare(SUBSETS[name](), 20_000, [1, 5_000, 20_000], split=split)
+
+
+@gpu
+@pytest.mark.parametrize("lanes", [0, 8])
+@pytest.mark.parametrize("split", [0.0, 0.3, 1e-300])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c4s"])
+def test_deterministic_record_layout(name, split, lanes):
+    """The record layout (D_v gathered from the coordinate record {x, abar, D, .}, no
+    per-entry D stream; hot-split features found in the block's shared-memory table,
+    including every feature hot): the same arithmetic as the oracle, long rows included."""
+    p = SUBSETS[name]()
+    _det_compare(p, 30_000, [1, 7_000, 30_000], split=split, lanes=lanes, record=True)
 
 
 @gpu
@@ -504,6 +521,58 @@ def test_async_sample_stream_and_quiescent_identity(name, bulk, split, repl, com
     ref_ab = A.T @ alpha / p.n
     assert rel(ab, ref_ab) <= 1e-10
     assert np.all(np.isfinite(x))
+
+
+@gpu
+@pytest.mark.parametrize("split", [0.0, 0.3])
+@pytest.mark.parametrize("name", ["c1", "c3s", "c4s"])
+def test_record_layout_async_stream_and_quiescent_identity(name, split):
+    """Record layout, async: every t processed once ((t, i_t) checksum), abar == (1/n) sum
+    alpha_i a_i once quiescent (each hot-split feature's adds reach its one home)."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 5 * p.n + 4321
+    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=256, record_samples=True, hot_split_min_freq=split,
+                             record_layout=True)
+    st = a.stats()
+    assert st["record_layout"] == 1
+    assert (st["hot_table_slots"] > 0) == (split > 0)
+    a.run(T, SEED)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, T, p.n)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x))
+    a.close()
+
+
+@gpu
+@pytest.mark.parametrize("conc", [16, 64])
+def test_record_layout_async_c1_within_1p5x_oracle(conc):
+    """Record layout, async on c1, one-epoch launches: epochs to 1e-6 within 1.5x the oracle's."""
+    m = asaga_mod()
+    p = datagen.make("c1")
+    fs = _fstar(p)
+    g = gamma_of(p)
+    st = oracle.State(p.n, p.d)
+    D = oracle.reweight(p.n, oracle.column_counts(p))
+
+    def orun(k):
+        oracle.sparse_saga(p, p.y, p.lam, g, SEED, k, st, D)
+        return oracle.objective(p, p.y, p.lam, st.x)
+
+    e_or = _epochs_to(p, fs, orun, launch=1.0)
+    a = m.Asaga.from_problem(p, g, concurrency=conc, hot_split_min_freq=0.3, record_layout=True)
+
+    def grun(k):
+        a.run(k, SEED)
+        return a.objective()
+
+    e_gpu = _epochs_to(p, fs, grun, launch=1.0)
+    a.close()
+    assert e_gpu <= 1.5 * e_or, (e_gpu, e_or)
 
 
 @gpu

@@ -42,6 +42,8 @@ def main():
     ap.add_argument("--pipe", type=float, default=0.0, help="pipe_late_min_freq (pipelined kernel)")
     ap.add_argument("--merge", type=int, default=0, help="pipe_merge_ns")
     ap.add_argument("--rowcp", action="store_true", help="row_copy_elementwise")
+    ap.add_argument("--overlap", type=int, default=0, help="measure_overlap (App. D counter every k-th sample)")
+    ap.add_argument("--record", action="store_true", help="record_layout (D from the coordinate record)")
     ap.add_argument("--launch", type=float, default=0.1,
                     help="epochs per asaga_run launch (f checked between launches): 0.1, or 1 as bench.py's value")
     ap.add_argument("--seeds", type=int, default=1, help="sample streams per point (seed, seed+1, ...)")
@@ -62,7 +64,8 @@ def main():
               combine_cluster=args.cluster, lanes_per_sample=args.lanes,
               combine_write_through=args.wt, combine_max_blocks=args.maxblocks,
               l2_persist_state=args.persist, pipe_late_min_freq=args.pipe,
-              pipe_merge_ns=args.merge, row_copy_elementwise=args.rowcp)
+              pipe_merge_ns=args.merge, row_copy_elementwise=args.rowcp, record_layout=args.record,
+              measure_overlap=args.overlap)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     grid = itertools.product([int(c) for c in args.conc.split(",")],
@@ -97,9 +100,12 @@ def main():
                     break
             st = a.stats()
             r = {"cfg": args.cfg, "W": st["concurrency"], "comb_H": st["combine_hot"], "cluster": st["combine_cluster"],
-                 "blocks": st["combine_blocks"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "pipe": args.pipe, "merge": args.merge, "split": args.split, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
+                 "blocks": st["combine_blocks"], "rec": st["record_layout"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "pipe": args.pipe, "merge": args.merge, "split": args.split, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
                  "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
                  "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
+            if args.overlap:
+                r["overlap_mean"], r["overlap_max"] = st["overlap_mean"], st["overlap_max"]
+                r["subopt"] = [float("%.3g" % f) for f in fs]
             if st["combine_passes"]:
                 r["comm_pass_us"] = last_ms * 1e3 * st["combine_blocks"] / st["combine_passes"]
             results.append(r)
