@@ -100,18 +100,24 @@ __device__ __forceinline__ double2 ld_na2(const double2* p) {
 // The 32-byte coordinate record {x_v, abar_v, D_v, .} (S >= 2): the {x, abar} pair and D_v
 // in ONE sector, gathered by a 128-bit and a 64-bit load (D_v is never written after A1)
 // -- D needs no per-entry stream.  (A single 256-bit load, LDG.E.NA.ENL2.256 on
-// sm_100, of the record was measured to break ASAGA's convergence on c3 -- f - f* stalls
-// at ~1e-4 with the hot split, with or without .STRONG.GPU -- while the deterministic
-// parity held: those loads are not used; profiles/r02_update_kernel.md.)
+// sm_100, ASAGA_REC256: same rate as the default layout on c4 and 15 epochs there, but on
+// c3 at 384 in flight the record layout -- with either load -- sits at a noise floor of
+// f - f* ~ 1e-4 unless the run is perturbed; profiles/r02_update_kernel.md section 7.)
 struct Rec3 {
   double x, ab, D;
 };
 __device__ __forceinline__ Rec3 ld_na_rec(const double2* p) {
-  const double2 a = ld_na2(p);
   Rec3 r;
+#ifdef ASAGA_REC256  // measurement variant only (profiles/r02_update_kernel.md section 7)
+  double s;
+  asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r.x), "=d"(r.ab), "=d"(r.D), "=d"(s) : "l"(p));
+#else
+  const double2 a = ld_na2(p);
   r.x = a.x;
   r.ab = a.y;
   r.D = ld_na(&p[1].x);
+#endif
   return r;
 }
 

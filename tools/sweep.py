@@ -103,9 +103,9 @@ def main():
                  "blocks": st["combine_blocks"], "rec": st["record_layout"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "pipe": args.pipe, "merge": args.merge, "split": args.split, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
                  "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
                  "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
+            r["subopt"] = [float("%.3g" % f) for f in fs]
             if args.overlap:
                 r["overlap_mean"], r["overlap_max"] = st["overlap_mean"], st["overlap_max"]
-                r["subopt"] = [float("%.3g" % f) for f in fs]
             if st["combine_passes"]:
                 r["comm_pass_us"] = last_ms * 1e3 * st["combine_blocks"] / st["combine_passes"]
             results.append(r)
