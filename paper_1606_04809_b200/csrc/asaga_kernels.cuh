@@ -358,6 +358,11 @@ __device__ __forceinline__ void report_body(const unsigned long long* __restrict
 // warp instructions per chunk on c4, ncu) become one warp sum per row (117 per chunk).
 enum : int { kIngestFlat = 0, kIngestStaged = 1, kIngestRows = 2 };
 constexpr int kStageCap = 512;  // entries per warp stage (int32 index + fp64 value: 6 KiB)
+#ifdef ASAGA_INGEST_ROWS_BLOCKING  // measurement variant: the blocking rows loop
+constexpr bool kIngestRowsPipe = false;
+#else
+constexpr bool kIngestRowsPipe = true;
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
@@ -474,6 +479,90 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         my_max = fmax(my_max, sq);
       }
       __syncwarp();  // the stage is refilled by the next tile
+      continue;
+    }
+    if (MODE == kIngestRows && kIngestRowsPipe) {
+      // software pipeline over the tile's row groups of kRQ x 32 entries: the next group (the
+      // rest of this row, or the start of the next one) is loaded into the second register
+      // set before the current group is checked and counted, so the loads of one group are in
+      // flight while the previous one is processed (the blocking version loaded 4 chunks,
+      // waited, processed: latency-bound, long-scoreboard stalls at one block per SM)
+      constexpr int kRQ = 2;
+      int32_t cA[kRQ], cB[kRQ];
+      double vA[kRQ], vB[kRQ];
+      auto load_group = [&](int64_t e00, int64_t rhi, int32_t (&cq)[kRQ], double (&vq)[kRQ]) {
+#pragma unroll
+        for (int qq = 0; qq < kRQ; ++qq) {
+          const int64_t e = e00 + 32 * qq + lane;
+          cq[qq] = e < rhi ? __ldcs(p.indices + e) : INT32_MAX;
+          vq[qq] = e < rhi ? __ldcs(p.data + e) : 0.0;
+        }
+      };
+      int jc = 0;
+      int64_t rlo = __shfl_sync(0xffffffffu, lo, 0);
+      int64_t ec = rlo, hc = __shfl_sync(0xffffffffu, hi, 0);
+      load_group(ec, hc, cA, vA);
+      int carry = -1;
+      double sq = 0.0;
+      bool br_any = false, bo_any = false, bv_any = false;
+      // one step: load the next group into (cn, vn), process (cc, vc); false after the last
+      // row.  Called alternately with the two register sets swapped (no register copies:
+      // a copy of a load's destination waits for the load -- 47 % of the stall samples)
+      auto step = [&](const int32_t (&cc)[kRQ], const double (&vc)[kRQ], int32_t (&cn)[kRQ],
+                      double (&vn)[kRQ]) -> bool {
+        int jn = jc;
+        int64_t en = ec + 32 * kRQ, hn = hc;
+        const bool row_end = en >= hc;  // warp-uniform
+        if (row_end) {
+          jn = jc + 1;
+          if (jn < nr) {
+            en = __shfl_sync(0xffffffffu, lo, jn);
+            hn = __shfl_sync(0xffffffffu, hi, jn);
+          }
+        }
+        if (jn < nr) load_group(en, hn, cn, vn);
+#pragma unroll
+        for (int qq = 0; qq < kRQ; ++qq) {
+          const int64_t e0 = ec + 32 * qq;
+          if (e0 >= hc) break;  // warp-uniform
+          const int64_t e = e0 + lane;
+          const int32_t c = cc[qq];
+          const double v = vc[qq];
+          int prev = __shfl_up_sync(0xffffffffu, c, 1);
+          if (lane == 0) prev = carry;
+          carry = __shfl_sync(0xffffffffu, c, 31);
+          if (e < hc) {
+            const bool br = (c < 0) || ((int64_t)c >= p.d);
+            br_any |= br;
+            bo_any |= e > rlo && prev >= c;
+            bv_any |= !isfinite(v);
+            sq = fma(v, v, sq);
+            if (!br) count_col(c);
+          }
+        }
+        if (row_end) {
+          sq = group_sum<32>(sq, 0xffffffffu);
+          const bool bad = __any_sync(0xffffffffu, br_any), bado = __any_sync(0xffffffffu, bo_any),
+                     badv = __any_sync(0xffffffffu, bv_any);
+          if (lane == jc) {
+            my_max = fmax(my_max, sq);
+            if (bad) atomicMin(&p.err_row[ERR_INDEX_RANGE], (unsigned long long)i);
+            if (bado) atomicMin(&p.err_row[ERR_INDEX_ORDER], (unsigned long long)i);
+            if (badv) atomicMin(&p.err_row[ERR_NONFINITE], (unsigned long long)i);
+          }
+          if (jn >= nr) return false;
+          carry = -1;
+          sq = 0.0;
+          br_any = bo_any = bv_any = false;
+          rlo = en;
+        }
+        jc = jn;
+        ec = en;
+        hc = hn;
+        return true;
+      };
+      while (step(cA, vA, cB, vB) && step(cB, vB, cA, vA)) {
+      }
       continue;
     }
     if (MODE == kIngestRows) {
@@ -2088,6 +2177,37 @@ margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict
       hi[u] = i < n ? rowptr[i + 1] : 0;
     }
     double m[U];
+    if (G == 32) {
+      // long rows: the first C chunks of all U rows are loaded before any use (U x C
+      // column loads, then U x C gathers of x in flight per lane; one row's chunks at a time
+      // left the warp waiting on its gathers: c4 1.55 ms)
+      constexpr int C = 4;
+      int c[U][C];
+      double a[U][C], xv[U][C];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < C; ++j) {
+          const int64_t k = lo[u] + j * G + g;
+          c[u][j] = k < hi[u] ? __ldcs(cols + k) : -1;
+          a[u][j] = k < hi[u] ? __ldcs(vals + k) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < C; ++j) xv[u][j] = c[u][j] >= 0 ? __ldg(x + (int64_t)xs * c[u][j]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        m[u] = 0.0;
+#pragma unroll
+        for (int j = 0; j < C; ++j) m[u] = fma(a[u][j], xv[u][j], m[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll 4
+        for (int64_t k = lo[u] + C * G + g; k < hi[u]; k += G) m[u] = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m[u]);
+      }
+    } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t k = lo[u] + g;
@@ -2097,6 +2217,7 @@ margin_rows_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict
     for (int u = 0; u < U; ++u) {
 #pragma unroll 4
       for (int64_t k = lo[u] + G + g; k < hi[u]; k += G) m[u] = fma(vals[k], __ldg(x + (int64_t)xs * cols[k]), m[u]);
+    }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
