@@ -165,6 +165,12 @@ __device__ __forceinline__ void st_cg(double* p, double v) {
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_u32(int32_t* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -363,6 +369,7 @@ constexpr bool kIngestRowsPipe = false;
 #else
 constexpr bool kIngestRowsPipe = true;
 #endif
+constexpr int kIngestPF = 512;  // rows-mode L2 prefetch distance (entries)
 
 template <int MODE>
 __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
@@ -394,7 +401,7 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
         k = prev == -1 ? c : prev;
       }
       if (k == c) atomicAdd(&hcnt[slot], 1);
-      else atomicAdd(&p.counts[c], 1);
+      else red_add_u32(p.counts + c, 1u);  // REDG: no response traffic (ATOMG returns a sector)
     }
   };
   if (p.smem_hist) {
@@ -521,6 +528,17 @@ __global__ void __launch_bounds__(1024) ingest_tile_kernel(IngestParams p) {
           }
         }
         if (jn < nr) load_group(en, hn, cn, vn);
+#ifndef ASAGA_INGEST_NO_PF
+        {  // L2 prefetch of the warp's entries kIngestPF ahead in the tile (rows are
+           // contiguous): the register loads one group ahead then come from L2
+          const int64_t pf = ec + kIngestPF;
+          if (lane < 8 && pf < end) {
+            const char* a = lane < 3 ? reinterpret_cast<const char*>(p.indices + pf) + lane * 128
+                                     : reinterpret_cast<const char*>(p.data + pf) + (lane - 3) * 128;
+            prefetch_l2(a);
+          }
+        }
+#endif
 #pragma unroll
         for (int qq = 0; qq < kRQ; ++qq) {
           const int64_t e0 = ec + 32 * qq;
