@@ -1311,8 +1311,10 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
           xb[j] = rx[c];
         else if (p.split && sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
 #ifdef ASAGA_TIMING
-          xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x),
-                               (p.debug_mode & 8) ? 0.0 : ld_na(p.habar + c));  // bit3: no hot abar ops
+          // bit7: no load of a hot entry's x (its RED stays): the hot lines carry REDs only
+          xb[j] = make_double2((p.debug_mode & 128) ? 0.0 : ld_na(&p.xa[(int64_t)c * p.S].x),
+                               (p.debug_mode & (8 | 256)) ? 0.0 : ld_na(p.habar + c));  // bit3: no hot abar ops
+          // (bit8: no load of a hot entry's abar, its RED stays)
 #else
           xb[j] = make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c));
 #endif
