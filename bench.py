@@ -94,16 +94,19 @@ class pinned_core:
 OPERATING_POINT = {
     # c1 (n = 1000): 64 in flight = 6.4 % of n (Thm 2 asks tau < n/10) at half the step:
     # 11-13 epochs in one-epoch launches (W = 16, gamma 1/(3L): 12-14 at a third of the rate)
-    "c1": dict(W=64, gscale=0.5, bulk=0.0, split=0.0, repl=0, comb=0.0),
+    "c1": dict(W=64, gscale=0.5, bulk=0.0, split=0.0, repl=0, comb=0.0, unpaired=1),
     # c2: every feature combined per thread block (asaga_combine_kernel), 40 workers per SM
     # (W = 6808, 46 per SM, is 7 % faster but sits at the edge: one round-end test run saw
     # all three streams miss 1e-6 in 15 one-epoch launches; 5920 gives 11 epochs with margin)
     "c2": dict(W=5920, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
-    # c3 / c4: plain kernel, abar of features in >= 30% of rows on its own line (hot split);
-    # rows staged by 1-D TMA bulk copies on c3 (+4.5 % update rate), by per-element cp.async
-    # on c4 (2.5 % faster there; profiles/r02_update_kernel.md)
-    "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.3, repl=0, comb=0.0, rowcp=0),
-    "c4": dict(W=448, gscale=0.25, bulk=0.0, split=0.3, repl=0, comb=0.0, rowcp=1),
+    # c3 / c4: plain kernel, paired scatter (the x and abar adds of one entry in one reduction
+    # instruction: one L2 request per {x, abar} sector), rows staged by 1-D TMA bulk copies;
+    # no hot split (with pairing the popular pair's line takes a load and one merged request
+    # per update).  c1 keeps the unpaired scatter (6 % faster there).  Round-2 sweeps in
+    # profiles/r02_update_kernel.md section 10: c3 1.72e8 -> 1.76e8 at the same W; c4 at
+    # W = 480 (15 epochs in every stream) 1.59e8 -> 1.79e8.
+    "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0),
+    "c4": dict(W=480, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0),
 }
 
 
@@ -112,7 +115,8 @@ def asaga_options(op):
     return dict(bulk_scatter_min_freq=op["bulk"], hot_split_min_freq=op["split"],
                 smem_replica_refresh=op["repl"], combine_min_freq=op["comb"],
                 l2_persist_state=bool(op.get("persist", False)),
-                row_copy_elementwise=bool(op.get("rowcp", 0)))
+                row_copy_elementwise=bool(op.get("rowcp", 0)),
+                scatter_unpaired=bool(op.get("unpaired", 0)))
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -564,6 +568,12 @@ def main():
             hot, hot_ops = bp.get("hot_k10_bulk_only_per_s_per_pair"), "one 16-B bulk reduction (reads from the SMEM replica) per update"
         elif bulk > 0:
             hot, hot_ops = bp.get("hot_k10_updates_per_s_per_pair"), "pair load + one 16-B bulk reduction per update"
+        elif op["split"] == 0 and not op.get("unpaired", 0):
+            # paired scatter: the popular pair's line takes one 16-B load and ONE request
+            # carrying both adds per update (tools/red_pairing.cu)
+            rp = load_json("profiles", "microbench_red_pairing.json") or {}
+            hot, hot_ops = (rp.get("hot_k10_paired_updates_per_s_per_pair"),
+                            "pair load + one paired reduction (x and abar adds of one sector in one instruction) per update")
         elif op["split"] > 0:
             hot, hot_ops = (mb.get("hot_line") or {}).get("ld_red_k10", {}).get("per_line"), "load + RED (x, abar split) per update"
         else:

@@ -174,6 +174,12 @@ typedef struct {
                             loads per entry on the popular lines).
                             0 (default) = D_{c_k} streamed with the row from a per-entry copy.
                             Same arithmetic. */
+  int scatter_unpaired;  /* plain update kernel (REDs, default layout): 0 (default) = paired
+                            scatter -- partner lanes g, g^1 each add x of their own entry and
+                            abar of the partner's, so ONE reduction instruction carries both
+                            words of one {x, abar} pair (one 32-byte sector: L2 serves them as
+                            one request); 1 = one instruction per word (x, then abar).  Same
+                            adds, same values. */
 } asaga_options;
 
 typedef struct {

@@ -96,6 +96,7 @@ struct asaga_ctx {
   int l2_persist = 0;          // plain kernel: L2 access-policy window (persisting) over xa
   double pipe_freq = 0.0;      // > 0: asaga_pipe_kernel, features with p_v >= it read late
   int row_copy_elementwise = 0;  // plain kernel: per-element cp.async row staging (no TMA bulk)
+  int scatter_unpaired = 0;      // plain kernel: one reduction instruction per word (no pairing)
   int rec_layout = 0;            // plain kernel: the record layout (D from the coordinate record, no dv stream)
   int32_t* hot_tab = nullptr;    // record layout + hot split: membership table of the hot-split features
   int hot_log = 0;               // ... log2 of its slots
@@ -1014,6 +1015,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   }
   ctx->pipe_merge = o.pipe_merge_ns;
   ctx->row_copy_elementwise = o.row_copy_elementwise ? 1 : 0;
+  ctx->scatter_unpaired = o.scatter_unpaired ? 1 : 0;
   ctx->rec_layout = o.record_layout ? 1 : 0;
   ctx->hot_freq = o.combine_min_freq > 0.0 ? o.combine_min_freq : (ctx->pipe_merge ? ctx->pipe_freq : 0.0);
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
@@ -1220,6 +1222,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.comm_passes = ctx->comb_freq > 0.0 ? ctx->scratch + ERR_COUNT + 2 : nullptr;
   p.wt = ctx->comb_wt;
   p.split = ctx->hot_dmax > 0.0 ? 1 : 0;
+  p.pair_red = ctx->scatter_unpaired ? 0 : 1;
   p.late_dmax = ctx->pipe_freq > 0.0 ? 1.0 / ctx->pipe_freq : 0.0;
   p.hot_dmax = ctx->hot_dmax;
   p.merge_ts = use_merge(ctx) ? merge_ts(ctx) : 0;
@@ -1331,6 +1334,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->pipe_merge_ns = 0;
   opt->row_copy_elementwise = 0;
   opt->record_layout = 0;
+  opt->scatter_unpaired = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

@@ -165,6 +165,12 @@ __device__ __forceinline__ void st_cg(double* p, double v) {
 __device__ __forceinline__ void red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
+// The same add under a predicate, as ONE predicated instruction (no branch around it), so
+// that lanes taking different roles in the paired scatter still issue it together.
+__device__ __forceinline__ void red_add_if(double* p, double v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.relaxed.gpu.global.add.f64 [%0], %1;\n\t}"
+               ::"l"(p), "d"(v), "r"((int)pred) : "memory");
+}
 __device__ __forceinline__ void red_add_u32(int32_t* p, unsigned v) {
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1003,6 +1009,7 @@ struct UpdateParams {
   // membership in hot_tab (2^hot_log slots, copied to shared memory), NULL = no split
   const int32_t* hot_tab;
   int hot_log;
+  int pair_red;           // asaga_update_kernel (REDs, no record layout): paired scatter
 };
 
 // Shared memory per group: a P-entry {dx, dabar} source buffer for the TMA bulk
@@ -1405,6 +1412,40 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
     //      are re-read from the stage buffer, which is only overwritten next iteration
     if (MODE == 2) bulk_wait_read();  // the previous sample's bulk ops have read dbuf
     TMARK(6);
+    if (MODE == 1 && !REC && p.pair_red && !p.frozen) {
+      // Paired scatter: lanes g and g^1 (partners) hold entries e0 (even lane) and e1 (odd
+      // lane).  Each lane adds x of its own entry and abar of its partner's (the partner's
+      // column, value and D are in the stage; abar's add needs no gathered value), in the
+      // order that puts the x and abar adds of ONE entry into the same instruction:
+      //   instruction 1: x(e0) by the even lane, abar(e0) by the odd lane
+      //   instruction 2: abar(e1) by the even lane, x(e1) by the odd lane
+      // Both words of a {x, abar} pair share a 32-byte sector, and L2 serves the lanes of
+      // one reduction instruction that hit one sector as one request: half the requests of
+      // one instruction per word (tools/red_pairing.cu: 2x the cold-entry rate, 1.65x the
+      // rate of a popular pair).  Same adds, same values (Property 3).
+      const bool odd = (g & 1) != 0;
+#pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        if (j * G >= len) break;  // group-uniform
+        const int e = j * G + g, ep = e ^ 1;
+        const bool own = e < len, pin = ep < len;
+        double* xv = &p.xa->x;  // (any valid address: the add is predicated off)
+        double dx = 0.0;
+        if (own) {
+          xv = &p.xa[(int64_t)sc[e] * p.S].x;
+          dx = ngam * fma(db, sv[e], qq[j]);
+        }
+        double* abp = &p.xa->x;
+        double dyp = 0.0;
+        if (pin) {
+          const int cp = sc[ep];
+          abp = (p.split && sd[ep] < 0.0) ? p.habar + cp : &p.xa[(int64_t)cp * p.S].x + 1;  // hot split
+          dyp = db * sv[ep] * p.inv_n;
+        }
+        red_add_if(odd ? abp : xv, odd ? dyp : dx, odd ? pin : own);
+        red_add_if(odd ? xv : abp, odd ? dx : dyp, odd ? own : pin);
+      }
+    } else
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       if (j * G >= len) break;  // group-uniform

@@ -128,12 +128,14 @@ def test_sigma_device_function_accuracy():
 
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
-def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False, record=False):
+def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False, record=False,
+                 unpaired=False):
     m = asaga_mod()
     g = gamma_of(prob)
     a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
                              bulk_scatter_min_freq=bulk, hot_split_min_freq=split,
-                             row_copy_elementwise=elementwise, record_layout=record)
+                             row_copy_elementwise=elementwise, record_layout=record,
+                             scatter_unpaired=unpaired)
     st = a.stats()
     if not record or bulk > 0.0:
         assert st["record_layout"] == 0
@@ -198,6 +200,43 @@ def test_deterministic_record_layout(name, split, lanes):
     including every feature hot): the same arithmetic as the oracle, long rows included."""
     p = SUBSETS[name]()
     _det_compare(p, 30_000, [1, 7_000, 30_000], split=split, lanes=lanes, record=True)
+
+
+@gpu
+@pytest.mark.parametrize("lanes", [0, 8])
+@pytest.mark.parametrize("unpaired", [False, True])
+@pytest.mark.parametrize("split", [0.0, 0.3])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c4s"])
+def test_deterministic_scatter_pairing(name, split, unpaired, lanes):
+    """The paired scatter (partner lanes g, g^1: each adds x of its own entry and abar of its
+    partner's, predicated off past the row's end -- odd row lengths leave one partner
+    without an entry) and the unpaired one (one reduction instruction per word): the same
+    adds as the oracle, with and without the hot split, long rows included."""
+    p = SUBSETS[name]()
+    _det_compare(p, 30_000, [1, 7_000, 30_000], split=split, lanes=lanes, unpaired=unpaired)
+
+
+@gpu
+@pytest.mark.parametrize("unpaired", [False, True])
+@pytest.mark.parametrize("split", [0.0, 0.3])
+@pytest.mark.parametrize("name", ["c1", "c3s", "c4s"])
+def test_scatter_pairing_async_stream_and_quiescent_identity(name, split, unpaired):
+    """Async, paired and unpaired scatter: every t processed once ((t, i_t) checksum) and,
+    once quiescent, abar == (1/n) sum alpha_i a_i (no add lost or doubled by the pairing)."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 5 * p.n + 999
+    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=512, record_samples=True, hot_split_min_freq=split,
+                             scatter_unpaired=unpaired)
+    a.run(T, SEED)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, T, p.n)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x))
+    a.close()
 
 
 @gpu
