@@ -105,7 +105,10 @@ OPERATING_POINT = {
     # per update).  c1 keeps the unpaired scatter (6 % faster there).  Round-2 sweeps in
     # profiles/r02_update_kernel.md section 10: c3 1.72e8 -> 1.76e8 at the same W; c4 at
     # W = 480 (15 epochs in every stream) 1.59e8 -> 1.79e8.
-    "c3": dict(W=384, gscale=0.3, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0),
+    # c3: the record layout ({x, abar, D, .} per coordinate: one 256-bit gather and one paired
+    # request per entry, no per-entry D stream, no expand pass) at W = 352: 1.87e8 in 12 epochs
+    # (the default layout: 1.76e8 at W = 384, 12 epochs; section 11 of the same file)
+    "c3": dict(W=352, gscale=0.3, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, rec=1),
     "c4": dict(W=480, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0),
 }
 
@@ -116,7 +119,8 @@ def asaga_options(op):
                 smem_replica_refresh=op["repl"], combine_min_freq=op["comb"],
                 l2_persist_state=bool(op.get("persist", False)),
                 row_copy_elementwise=bool(op.get("rowcp", 0)),
-                scatter_unpaired=bool(op.get("unpaired", 0)))
+                scatter_unpaired=bool(op.get("unpaired", 0)),
+                record_layout=bool(op.get("rec", 0)))
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -617,10 +621,12 @@ def main():
             # ours per step: ingest_init (not for d <= 1024: the ingest initialises itself),
             # ingest (for d <= 4096 its last block also runs the profile and the report; else
             # profile + report kernels, and A9's dense copy of x), update, margin (its last
-            # block finishes f), + expand_d unless every feature is combined, + hot_flag and
+            # block finishes f), + expand_d unless every feature is combined or the record layout
+            # carries D, + hot_flag and
             # hot_slot when combining with d > 4096 (CUB's scan kernels are library)
             "gpu_launches": (4 - (1 if p.d <= 1024 else 0) + (0 if p.d <= 4096 else 3)
-                             + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) else 1)
+                             + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) or st_timed["record_layout"]
+                                else 1)
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),
         }

@@ -98,21 +98,21 @@ __device__ __forceinline__ double2 ld_na2(const double2* p) {
   return v;
 }
 // The 32-byte coordinate record {x_v, abar_v, D_v, .} (S >= 2): the {x, abar} pair and D_v
-// in ONE sector, gathered by a 128-bit and a 64-bit load (D_v is never written after A1)
-// -- D needs no per-entry stream.  (A single 256-bit load, LDG.E.NA.ENL2.256 on
-// sm_100, ASAGA_REC256: same rate as the default layout on c4 and 15 epochs there, but on
-// c3 at 384 in flight the record layout -- with either load -- sits at a noise floor of
-// f - f* ~ 1e-4 unless the run is perturbed; profiles/r02_update_kernel.md section 7.)
+// in ONE sector, gathered by one 256-bit load (LDG.E.NA.ENL2.256 on sm_100; D_v is never
+// written after A1) -- D needs no per-entry stream.  ASAGA_REC_TWO_LOADS (measurement
+// variant): a 128-bit and a 64-bit load.  (Round 2: on c3 at 384 in flight the record layout
+// -- with either load -- sat at a noise floor of f - f* ~ 1e-4 unless the run was perturbed;
+// profiles/r02_update_kernel.md sections 7 and 11.)
 struct Rec3 {
   double x, ab, D;
 };
 __device__ __forceinline__ Rec3 ld_na_rec(const double2* p) {
   Rec3 r;
-#ifdef ASAGA_REC256  // measurement variant only (profiles/r02_update_kernel.md section 7)
+#ifndef ASAGA_REC_TWO_LOADS  // one 256-bit load: one request for the record's sector
   double s;
   asm volatile("ld.global.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(r.x), "=d"(r.ab), "=d"(r.D), "=d"(s) : "l"(p));
-#else
+#else  // measurement variant: {x, abar} + D (profiles/r02_update_kernel.md section 7)
   const double2 a = ld_na2(p);
   r.x = a.x;
   r.ab = a.y;
@@ -1412,7 +1412,7 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
     //      are re-read from the stage buffer, which is only overwritten next iteration
     if (MODE == 2) bulk_wait_read();  // the previous sample's bulk ops have read dbuf
     TMARK(6);
-    if (MODE == 1 && !REC && p.pair_red && !p.frozen) {
+    if (MODE == 1 && (!REC || p.hot_tab == nullptr) && p.pair_red && !p.frozen) {
       // Paired scatter: lanes g and g^1 (partners) hold entries e0 (even lane) and e1 (odd
       // lane).  Each lane adds x of its own entry and abar of its partner's (the partner's
       // column, value and D are in the stage; abar's add needs no gathered value), in the
@@ -1439,7 +1439,7 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
         double dyp = 0.0;
         if (pin) {
           const int cp = sc[ep];
-          abp = (p.split && sd[ep] < 0.0) ? p.habar + cp : &p.xa[(int64_t)cp * p.S].x + 1;  // hot split
+          abp = (!REC && p.split && sd[ep] < 0.0) ? p.habar + cp : &p.xa[(int64_t)cp * p.S].x + 1;  // hot split
           dyp = db * sv[ep] * p.inv_n;
         }
         red_add_if(odd ? abp : xv, odd ? dyp : dx, odd ? pin : own);
