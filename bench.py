@@ -109,7 +109,11 @@ OPERATING_POINT = {
     # request per entry, no per-entry D stream, no expand pass) at W = 352: 1.87e8 in 12 epochs
     # (the default layout: 1.76e8 at W = 384, 12 epochs; section 11 of the same file)
     "c3": dict(W=352, gscale=0.3, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, rec=1),
-    "c4": dict(W=480, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0),
+    # c4: D_c gathered per entry from the d-vector with the coordinate gather (d_gather: no
+    # per-entry D stream, no expand pass per reload -- 1.07 ms of the step) at W = 512: 1.74e8
+    # in 15 epochs (W = 544 needs 18-20); with the D stream the kernel peaks at 1.80e8 (W = 480)
+    # but the step pays the expand pass (section 15 of the same file)
+    "c4": dict(W=512, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, dgather=1),
 }
 
 
@@ -120,7 +124,7 @@ def asaga_options(op):
                 l2_persist_state=bool(op.get("persist", False)),
                 row_copy_elementwise=bool(op.get("rowcp", 0)),
                 scatter_unpaired=bool(op.get("unpaired", 0)),
-                record_layout=bool(op.get("rec", 0)))
+                record_layout=bool(op.get("rec", 0)), d_gather=bool(op.get("dgather", 0)))
 
 
 def hbm_bytes_per_update(mean_s: float) -> float:
@@ -621,12 +625,12 @@ def main():
             # ours per step: ingest_init (not for d <= 1024: the ingest initialises itself),
             # ingest (for d <= 4096 its last block also runs the profile and the report; else
             # profile + report kernels, and A9's dense copy of x), update, margin (its last
-            # block finishes f), + expand_d unless every feature is combined or the record layout
-            # carries D, + hot_flag and
+            # block finishes f), + expand_d unless every feature is combined, the record layout
+            # carries D or the kernel gathers it (d_gather), + hot_flag and
             # hot_slot when combining with d > 4096 (CUB's scan kernels are library)
             "gpu_launches": (4 - (1 if p.d <= 1024 else 0) + (0 if p.d <= 4096 else 3)
                              + (0 if (op["comb"] > 0 and st_timed["combine_hot"] == p.d) or st_timed["record_layout"]
-                                else 1)
+                                or op.get("dgather", 0) else 1)
                              + (2 if op["comb"] > 0 and p.d > 4096 else 0)) * args.steps,
             "clocks": clk.summary(),
         }

@@ -180,6 +180,11 @@ typedef struct {
                             words of one {x, abar} pair (one 32-byte sector: L2 serves them as
                             one request); 1 = one instruction per word (x, then abar).  Same
                             adds, same values. */
+  int d_gather;          /* plain update kernel (REDs, default layout, no hot split, no replica):
+                            1 = D_c = n/n_c is gathered from the d-vector (read-only path) with
+                            each entry's coordinate gather, so there is no per-entry D array
+                            (nnz x 8 bytes) and no expand pass per reload.  0 (default) = D_c
+                            streamed with the row from the per-entry copy.  Same arithmetic. */
 } asaga_options;
 
 typedef struct {

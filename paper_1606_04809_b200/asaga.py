@@ -50,7 +50,8 @@ class Options(ctypes.Structure):
                 ("combine_max_blocks", ctypes.c_int), ("l2_persist_state", ctypes.c_int),
                 ("pipe_late_min_freq", ctypes.c_double), ("pipe_merge_ns", ctypes.c_int),
                 ("row_copy_elementwise", ctypes.c_int),
-                ("record_layout", ctypes.c_int), ("scatter_unpaired", ctypes.c_int)]
+                ("record_layout", ctypes.c_int), ("scatter_unpaired", ctypes.c_int),
+                ("d_gather", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -184,7 +185,8 @@ class Asaga:
                  combine_write_through: bool = False, combine_max_blocks: int = 0,
                  l2_persist_state: bool = False, pipe_late_min_freq: float = 0.0,
                  pipe_merge_ns: int = 0, row_copy_elementwise: bool = False,
-                 record_layout: bool = False, scatter_unpaired: bool = False):
+                 record_layout: bool = False, scatter_unpaired: bool = False,
+                 d_gather: bool = False):
         n = int(indptr.shape[0]) - 1
         nnz = int(indices.shape[0])
         device_inputs = _is_cuda(indptr)
@@ -216,6 +218,7 @@ class Asaga:
         opt.row_copy_elementwise = int(bool(row_copy_elementwise))
         opt.record_layout = int(bool(record_layout))
         opt.scatter_unpaired = int(bool(scatter_unpaired))
+        opt.d_gather = int(bool(d_gather))
         h = ctypes.c_void_p()
         fn = _lib.asaga_init_device if device_inputs else _lib.asaga_init
         st = fn(ctypes.byref(h), ctypes.byref(view), _ptr(y), float(lam), float(gamma),

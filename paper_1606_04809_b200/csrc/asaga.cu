@@ -97,6 +97,7 @@ struct asaga_ctx {
   double pipe_freq = 0.0;      // > 0: asaga_pipe_kernel, features with p_v >= it read late
   int row_copy_elementwise = 0;  // plain kernel: per-element cp.async row staging (no TMA bulk)
   int scatter_unpaired = 0;      // plain kernel: one reduction instruction per word (no pairing)
+  int d_gather = 0;              // plain kernel: D_c gathered per entry (no dv stream)
   int rec_layout = 0;            // plain kernel: the record layout (D from the coordinate record, no dv stream)
   int32_t* hot_tab = nullptr;    // record layout + hot split: membership table of the hot-split features
   int hot_log = 0;               // ... log2 of its slots
@@ -455,6 +456,12 @@ bool use_rec(const asaga_ctx* ctx) {
   return ctx->rec_layout && !use_pipe(ctx) && !use_combine(ctx) && scatter_mode(ctx) == 1 && !use_replica(ctx) &&
          ctx->S >= 2 && (ctx->hot_dmax == 0.0 || ctx->hot_tab != nullptr);
 }
+// d_gather: the plain kernel (REDs, default layout, no hot split, no replica) gathers D_c from
+// the d-vector with each entry's coordinate gather: no per-entry D stream, no expand pass.
+bool use_dg(const asaga_ctx* ctx) {
+  return ctx->d_gather && !ctx->rec_layout && !use_pipe(ctx) && !use_combine(ctx) && scatter_mode(ctx) == 1 &&
+         !use_replica(ctx) && ctx->hot_dmax == 0.0;
+}
 size_t rec_tab_bytes(const asaga_ctx* ctx) {  // the kernel's shared copy of the table
   return ctx->hot_tab != nullptr ? (size_t)sizeof(int32_t) << ctx->hot_log : 0;
 }
@@ -807,7 +814,7 @@ asaga_status enqueue_report(asaga_ctx* ctx, bool guard) {
 // D per stored entry: read by the plain kernel and by the combine kernel unless every feature
 // is hot (D from its block table); the pipelined kernel gathers D_v from the d-vector itself
 bool needs_dv(const asaga_ctx* ctx) {
-  return !(use_combine(ctx) && ctx->comb_H == ctx->d) && !use_pipe(ctx) && !use_rec(ctx);
+  return !(use_combine(ctx) && ctx->comb_H == ctx->d) && !use_pipe(ctx) && !use_rec(ctx) && !use_dg(ctx);
 }
 
 // D per stored entry (+ the entry's combine slot): every kernel but the combine kernel
@@ -1016,6 +1023,7 @@ asaga_status make_ctx(asaga_ctx** out, const asaga_csr_view* A, const double* y,
   ctx->pipe_merge = o.pipe_merge_ns;
   ctx->row_copy_elementwise = o.row_copy_elementwise ? 1 : 0;
   ctx->scatter_unpaired = o.scatter_unpaired ? 1 : 0;
+  ctx->d_gather = o.d_gather ? 1 : 0;
   ctx->rec_layout = o.record_layout ? 1 : 0;
   ctx->hot_freq = o.combine_min_freq > 0.0 ? o.combine_min_freq : (ctx->pipe_merge ? ctx->pipe_freq : 0.0);
   ctx->comb_wt = o.combine_write_through ? 1 : 0;
@@ -1188,7 +1196,7 @@ asaga_status enqueue_run(asaga_ctx* ctx, uint64_t n_updates, uint64_t seed, bool
   p.cols = ctx->cols;
   p.vals = ctx->vals;
   p.y = ctx->y;
-  p.dv = use_rec(ctx) ? nullptr : ctx->dv;
+  p.dv = (use_rec(ctx) || use_dg(ctx)) ? nullptr : ctx->dv;
   p.D = ctx->D;
   p.xa = ctx->xa;
   p.S = ctx->S;
@@ -1335,6 +1343,7 @@ void asaga_options_default(asaga_options* opt) {
   opt->row_copy_elementwise = 0;
   opt->record_layout = 0;
   opt->scatter_unpaired = 0;
+  opt->d_gather = 0;
 }
 
 asaga_status asaga_init(asaga_ctx** out, const asaga_csr_view* A, const double* y, double lambda,

@@ -1314,6 +1314,7 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
       const int64_t k = lo + j * G + g;
       if (j * G + g < len) {
         const int c = sc[j * G + g];
+        if (!REC && dvs == nullptr) qq[j] = __ldg(p.D + c);  // d_gather: D_c with the gather
         if (REPL)
           xb[j] = rx[c];
         else if (p.split && sd[j * G + g] < 0.0)  // hot split: x and abar on separate lines
@@ -1369,7 +1370,7 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
         if (REC)
           qq[j] = Dr[j] * fma(p.lambda_, xb[j].x, ((hm >> j) & 1u) ? hb[j] : xb[j].y);
         else
-          qq[j] = fabs(sd[j * G + g]) * fma(p.lambda_, xb[j].x, xb[j].y);
+          qq[j] = (dvs == nullptr ? qq[j] : fabs(sd[j * G + g])) * fma(p.lambda_, xb[j].x, xb[j].y);
       }
     }
     if (len > P)  // group-uniform: long rows only
@@ -1384,7 +1385,7 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
         qs[k - lo - P] = r.D * fma(p.lambda_, r.x, ab);
         continue;
       }
-      const double Dv = ld_nc_f64(p.dv + k);
+      const double Dv = dvs == nullptr ? __ldg(p.D + c) : ld_nc_f64(p.dv + k);
       const double2 v = REPL ? rx[c]
                         : Dv < 0.0 ? make_double2(ld_na(&p.xa[(int64_t)c * p.S].x), ld_na(p.habar + c))
                                    : ld_na2(p.xa + (int64_t)c * p.S);
@@ -1495,7 +1496,8 @@ __global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdatePa
       const double a = ld_nc_f64(p.vals + k);
       const double u = fma(db, a, qs[k - lo - P]);
       double* xv = &p.xa[(int64_t)c * p.S].x;
-      const bool hot = REC ? (p.hot_tab != nullptr && hot_lookup(ht, p.hot_log, c)) : ld_nc_f64(p.dv + k) < 0.0;
+      const bool hot = REC ? (p.hot_tab != nullptr && hot_lookup(ht, p.hot_log, c))
+                           : (dvs != nullptr && ld_nc_f64(p.dv + k) < 0.0);
       double* abv = hot ? p.habar + c : xv + 1;  // hot split
       if (ATOMIC) {
         red_add(xv, ngam * u);

@@ -129,13 +129,13 @@ def test_sigma_device_function_accuracy():
 
 # ---------------------------------------------------------------------- A2..A8 deterministic
 def _det_compare(prob, T, checkpoints, lanes=0, tol=1e-9, bulk=0.0, split=0.0, elementwise=False, record=False,
-                 unpaired=False):
+                 unpaired=False, d_gather=False):
     m = asaga_mod()
     g = gamma_of(prob)
     a = m.Asaga.from_problem(prob, g, deterministic=True, lanes_per_sample=lanes,
                              bulk_scatter_min_freq=bulk, hot_split_min_freq=split,
                              row_copy_elementwise=elementwise, record_layout=record,
-                             scatter_unpaired=unpaired)
+                             scatter_unpaired=unpaired, d_gather=d_gather)
     st = a.stats()
     if not record or bulk > 0.0:
         assert st["record_layout"] == 0
@@ -214,6 +214,36 @@ def test_deterministic_scatter_pairing(name, split, unpaired, lanes):
     adds as the oracle, with and without the hot split, long rows included."""
     p = SUBSETS[name]()
     _det_compare(p, 30_000, [1, 7_000, 30_000], split=split, lanes=lanes, unpaired=unpaired)
+
+
+@gpu
+@pytest.mark.parametrize("elementwise", [False, True])
+@pytest.mark.parametrize("unpaired", [False, True])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c4s"])
+def test_deterministic_d_gather(name, unpaired, elementwise):
+    """D_c gathered per entry from the d-vector (no per-entry D stream, no expand pass): the
+    same arithmetic as the oracle, long rows (the overflow loop) included."""
+    p = SUBSETS[name]()
+    _det_compare(p, 30_000, [1, 7_000, 30_000], unpaired=unpaired, elementwise=elementwise, d_gather=True)
+
+
+@gpu
+@pytest.mark.parametrize("name", ["c1", "c3s", "c4s"])
+def test_d_gather_async_stream_and_quiescent_identity(name):
+    """d_gather, async: every t processed once, abar == (1/n) sum alpha_i a_i once quiescent."""
+    import scipy.sparse
+
+    m = asaga_mod()
+    p = SUBSETS[name]()
+    T = 5 * p.n + 555
+    a = m.Asaga.from_problem(p, gamma_of(p), concurrency=512, record_samples=True, d_gather=True)
+    a.run(T, SEED)
+    assert a.sample_hash() == sample_hash_ref(SEED, 0, T, p.n)
+    x, alpha, ab, _ = a.get_state()
+    A = scipy.sparse.csr_matrix((p.data, p.indices, p.indptr), shape=(p.n, p.d))
+    assert rel(ab, A.T @ alpha / p.n) <= 1e-10
+    assert np.all(np.isfinite(x))
+    a.close()
 
 
 @gpu

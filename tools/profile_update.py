@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--rowcp", action="store_true", help="row_copy_elementwise")
     ap.add_argument("--unpaired", action="store_true", help="scatter_unpaired")
     ap.add_argument("--record", action="store_true", help="record_layout")
+    ap.add_argument("--dgather", action="store_true", help="d_gather")
     args = ap.parse_args()
     import torch
     from paper_1606_04809_b200 import Asaga
@@ -38,7 +39,7 @@ def main():
               hot_split_min_freq=args.split,
               smem_replica_refresh=args.repl, combine_min_freq=args.comb,
               pipe_late_min_freq=args.pipe, row_copy_elementwise=args.rowcp,
-              scatter_unpaired=args.unpaired, record_layout=args.record)
+              scatter_unpaired=args.unpaired, record_layout=args.record, d_gather=args.dgather)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     T = args.updates or p.n
     a.run(T, datagen.SAMPLE_SEED)  # warm-up launch

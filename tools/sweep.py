@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--overlap", type=int, default=0, help="measure_overlap (App. D counter every k-th sample)")
     ap.add_argument("--record", action="store_true", help="record_layout (D from the coordinate record)")
     ap.add_argument("--unpaired", action="store_true", help="scatter_unpaired (one reduction instruction per word)")
+    ap.add_argument("--dgather", action="store_true", help="d_gather (D_c gathered per entry, no D stream)")
     ap.add_argument("--launch", type=float, default=0.1,
                     help="epochs per asaga_run launch (f checked between launches): 0.1, or 1 as bench.py's value")
     ap.add_argument("--seeds", type=int, default=1, help="sample streams per point (seed, seed+1, ...)")
@@ -66,7 +67,7 @@ def main():
               combine_write_through=args.wt, combine_max_blocks=args.maxblocks,
               l2_persist_state=args.persist, pipe_late_min_freq=args.pipe,
               pipe_merge_ns=args.merge, row_copy_elementwise=args.rowcp, record_layout=args.record,
-              scatter_unpaired=args.unpaired, measure_overlap=args.overlap)
+              scatter_unpaired=args.unpaired, d_gather=args.dgather, measure_overlap=args.overlap)
     gamma0 = 1.0 / (3.0 * base.stats()["L"])
     results = []
     grid = itertools.product([int(c) for c in args.conc.split(",")],
@@ -101,7 +102,7 @@ def main():
                     break
             st = a.stats()
             r = {"cfg": args.cfg, "W": st["concurrency"], "comb_H": st["combine_hot"], "cluster": st["combine_cluster"],
-                 "blocks": st["combine_blocks"], "rec": st["record_layout"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "pipe": args.pipe, "unpaired": args.unpaired, "merge": args.merge, "split": args.split, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
+                 "blocks": st["combine_blocks"], "rec": st["record_layout"], "lanes": st["lanes_per_sample"], "gamma_scale": sc, "pipe": args.pipe, "unpaired": args.unpaired, "dgather": args.dgather, "merge": args.merge, "split": args.split, "seed_offset": sd, "launch_epochs": per, "epochs_to_tol": ep,
                  "updates_per_s": len(fs) * step / (upd_ms / 1e3), "time_to_tol_s": upd_ms / 1e3 if isinstance(ep, float) else None,
                  "oracle_epochs": gold["oracle_epochs_to_1e-6"], "subopt_last": fs[-1]}
             r["subopt"] = [float("%.3g" % f) for f in fs]
