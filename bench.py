@@ -110,10 +110,10 @@ OPERATING_POINT = {
     # (the default layout: 1.76e8 at W = 384, 12 epochs; section 11 of the same file)
     "c3": dict(W=352, gscale=0.3, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, rec=1),
     # c4: D_c gathered per entry from the d-vector with the coordinate gather (d_gather: no
-    # per-entry D stream, no expand pass per reload -- 1.07 ms of the step) at W = 512: 1.74e8
-    # in 15 epochs (W = 544 needs 18-20); with the D stream the kernel peaks at 1.80e8 (W = 480)
-    # but the step pays the expand pass (section 15 of the same file)
-    "c4": dict(W=512, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, dgather=1),
+    # per-entry D stream, no expand pass per reload -- 1.07 ms of the step) at W = 480: 1.78e8
+    # in 15 epochs (W = 544 does not converge); with the D stream the kernel reaches 1.82e8 but
+    # the step pays the expand pass (sections 15 and 18 of the same file)
+    "c4": dict(W=480, gscale=0.25, bulk=0.0, split=0.0, repl=0, comb=0.0, rowcp=0, dgather=1),
 }
 
 

@@ -1165,7 +1165,15 @@ __device__ unsigned long long g_phase_cycles[12];
 // chunk instead of 4, so one resident 256-thread block per SM -- 8 samples, beyond the
 // ~3 per SM the convergent concurrency asks for -- and no spills at NR = 8)
 template <int G, int NR, bool DET, int MODE, bool REPL, bool REC>
-__global__ void __launch_bounds__(256, REC ? 1 : 2) asaga_update_kernel(UpdateParams p) {
+// One resident 256-thread block per SM is all the launch shape uses (the convergent numbers
+// in flight are 3-4 groups per SM), so the register cap is 255: at the former cap of 128
+// (2 blocks per SM) the kernel spilled as soon as anything was added, and ran ~2 % slower on
+// c4 at 128 (profiles/r02_update_kernel.md section 18).  ASAGA_UPD_MIN_BLOCKS: measurement
+// variant.
+#ifndef ASAGA_UPD_MIN_BLOCKS
+#define ASAGA_UPD_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(256, ASAGA_UPD_MIN_BLOCKS) asaga_update_kernel(UpdateParams p) {
   constexpr bool ATOMIC = MODE != 0;
   static_assert(!REC || (MODE == 1 && !REPL), "record layout: REDs, no replica");
   if (p.ok != nullptr && *reinterpret_cast<const volatile int*>(p.ok) == 0) return;  // run guard
