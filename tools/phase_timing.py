@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--repl", type=int, default=0, help="smem_replica_refresh")
     ap.add_argument("--pipe", type=float, default=0.0, help="pipe_late_min_freq")
     ap.add_argument("--merge", type=int, default=0, help="pipe_merge_ns")
+    ap.add_argument("--dgather", action="store_true", help="d_gather")
+    ap.add_argument("--record", action="store_true", help="record_layout")
     args = ap.parse_args()
     import importlib.util
 
@@ -48,7 +50,7 @@ def main():
               bulk_scatter_min_freq=args.bulk,
               hot_split_min_freq=args.split,
               smem_replica_refresh=args.repl, pipe_late_min_freq=args.pipe,
-              pipe_merge_ns=args.merge)
+              pipe_merge_ns=args.merge, d_gather=args.dgather, record_layout=args.record)
     a.set_gamma(args.gscale / (3.0 * a.stats()["L"]))
     buf = (ctypes.c_ulonglong * 9)()
     names = ["row_wait", "gather_dot", "reduce_exp", "scatter", "tail", "-", "s_wait_read", "s_compute",
