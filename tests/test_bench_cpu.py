@@ -27,3 +27,21 @@ def test_bench_reference_nonzero_rank_is_silent():
                           "--workload", "c1", "--steps", "1", "--warmup", "1"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_operating_points_map_to_asaga_options():
+    """Every bench operating point translates into keyword options the binding accepts (a
+    renamed option would otherwise only fail on the GPU box)."""
+    import inspect
+
+    import bench
+    from paper_1606_04809_b200 import Asaga
+
+    params = inspect.signature(Asaga.__init__).parameters
+    assert set(bench.OPERATING_POINT) == {"c1", "c2", "c3", "c4"}
+    for name, op in bench.OPERATING_POINT.items():
+        kw = bench.asaga_options(op)
+        for k in kw:
+            assert k in params, (name, k)
+        assert op["W"] > 0 and 0.0 < op["gscale"] <= 1.0
+    assert bench.default_workload(1) == "c4" and bench.default_workload(8) == "c3"
