@@ -98,7 +98,10 @@ OPERATING_POINT = {
     # c2: every feature combined per thread block (asaga_combine_kernel), 40 workers per SM
     # (W = 6808, 46 per SM, is 7 % faster but sits at the edge: one round-end test run saw
     # all three streams miss 1e-6 in 15 one-epoch launches; 5920 gives 11 epochs with margin)
-    "c2": dict(W=5920, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
+    # (last session: with the final build's 1.3 us communication pass, W = 6512 reaches 1e-6 in
+    # 10 epochs in every stream, 3.76e9 /s; 6808: 11 epochs, 3.85e9, gamma window 0.04 only;
+    # profiles/r02_update_kernel.md section 22)
+    "c2": dict(W=6512, gscale=0.04, bulk=0.0, split=0.0, repl=0, comb=1e-300),
     # c3 / c4: plain kernel, paired scatter (the x and abar adds of one entry in one reduction
     # instruction: one L2 request per {x, abar} sector), rows staged by 1-D TMA bulk copies;
     # no hot split (with pairing the popular pair's line takes a load and one merged request
