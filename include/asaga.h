@@ -170,8 +170,10 @@ typedef struct {
                             PAPER.md:108-110) and the gather of an entry returns D_v with x and
                             abar from the same sector: no per-entry D array (nnz x 8 bytes) and
                             no expand pass per reload; the hot split's features are found in a
-                            per-block shared-memory table.  Measured slower on c3 / c4 (two
-                            loads per entry on the popular lines).
+                            per-block shared-memory table.  The record is gathered with one
+                            256-bit load and, without the hot split, scattered with the paired
+                            reductions: c3's operating point; slower on c4,
+                            whose 3.2M records (103 MB) crowd the L2.
                             0 (default) = D_{c_k} streamed with the row from a per-entry copy.
                             Same arithmetic. */
   int scatter_unpaired;  /* plain update kernel (REDs, default layout): 0 (default) = paired
@@ -183,8 +185,10 @@ typedef struct {
   int d_gather;          /* plain update kernel (REDs, default layout, no hot split, no replica):
                             1 = D_c = n/n_c is gathered from the d-vector (read-only path) with
                             each entry's coordinate gather, so there is no per-entry D array
-                            (nnz x 8 bytes) and no expand pass per reload.  0 (default) = D_c
-                            streamed with the row from the per-entry copy.  Same arithmetic. */
+                            (nnz x 8 bytes) and no expand pass per reload (c4's operating point).
+                            Ignored where it does not apply (record layout, hot split, replica,
+                            combine or pipelined kernel).  0 (default) = D_c streamed with the
+                            row from the per-entry copy.  Same arithmetic. */
 } asaga_options;
 
 typedef struct {
