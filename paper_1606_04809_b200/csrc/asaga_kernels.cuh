@@ -1438,18 +1438,33 @@ __global__ void __launch_bounds__(256, ASAGA_UPD_MIN_BLOCKS) asaga_update_kernel
         if (j * G >= len) break;  // group-uniform
         const int e = j * G + g, ep = e ^ 1;
         const bool own = e < len, pin = ep < len;
-        double* xv = &p.xa->x;  // (any valid address: the add is predicated off)
-        double dx = 0.0;
-        if (own) {
-          xv = &p.xa[(int64_t)sc[e] * p.S].x;
+        double* xv;
+        double* abp;
+        double dx, dyp;
+        if (REC) {
+          // branch-free (the record layout has no hot split here): the stage's slots past the
+          // row's end hold stale data, never dereferenced -- those lanes' reductions are
+          // predicated off.  The scatter phase halves (c3: 1.87e8 -> 1.94e8); on the default
+          // layout (c4) the same form is slower (profiles/r02_update_kernel.md section 24).
+          const int c = sc[e], cp = sc[ep];
+          xv = &p.xa[(int64_t)c * p.S].x;
+          abp = &p.xa[(int64_t)cp * p.S].x + 1;
           dx = ngam * fma(db, sv[e], qq[j]);
-        }
-        double* abp = &p.xa->x;
-        double dyp = 0.0;
-        if (pin) {
-          const int cp = sc[ep];
-          abp = (!REC && p.split && sd[ep] < 0.0) ? p.habar + cp : &p.xa[(int64_t)cp * p.S].x + 1;  // hot split
           dyp = db * sv[ep] * p.inv_n;
+        } else {
+          xv = &p.xa->x;  // (any valid address: the add is predicated off)
+          dx = 0.0;
+          if (own) {
+            xv = &p.xa[(int64_t)sc[e] * p.S].x;
+            dx = ngam * fma(db, sv[e], qq[j]);
+          }
+          abp = &p.xa->x;
+          dyp = 0.0;
+          if (pin) {
+            const int cp = sc[ep];
+            abp = (p.split && sd[ep] < 0.0) ? p.habar + cp : &p.xa[(int64_t)cp * p.S].x + 1;  // hot split
+            dyp = db * sv[ep] * p.inv_n;
+          }
         }
         red_add_if(odd ? abp : xv, odd ? dyp : dx, odd ? pin : own);
         red_add_if(odd ? xv : abp, odd ? dx : dyp, odd ? own : pin);
